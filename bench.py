@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark driver: Dphi GFLOP/s and CG time-to-solution on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+Mirrors the reference's Dirac kernel benchmark (proj/src/bench.cpp:190-248:
+FLOPs = flops_per_site x global volume x applications, exact integers) on
+BASELINE.json's configs (default: configs[1], SU(2) fundamental 32^4, the
+config the metric is quoted on at N = 1). A step is one full Dphi
+application over the lattice, inputs resident in HBM. One JSON line on rank 0.
+
+Under torchrun (N > 1) each rank owns one GPU and one sub-lattice (T split
+first, then Z: SURVEY.md §8e); halos move through the library's NCCL
+transport; time is the max over ranks of CUDA-event time.
+
+--impl reference times the reference's own CPU apply_dirac (oracle/_ref, the
+unmodified latbench compiled from its sources) with all host threads on the
+same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs: (name, lattice T,X,Y,Z, N, rep, m0, links, cg tol)
+CONFIGS = {
+    1: dict(name="cfg1 SU(3)F 8^4", L=[8, 8, 8, 8], n=3, rep=0, mass=0.1, links="haar", tol=1e-10),
+    2: dict(name="cfg2 SU(2)F 32^4", L=[32, 32, 32, 32], n=2, rep=0, mass=0.05, links="haar", tol=1e-10),
+    3: dict(name="cfg3 SU(3)F 96x48^3 near-unit", L=[96, 48, 48, 48], n=3, rep=0, mass=0.02,
+            links="near_unit", tol=1e-12),
+    4: dict(name="cfg4 SU(2)A 40^4", L=[40, 40, 40, 40], n=2, rep=1, mass=0.05, links="haar", tol=1e-10),
+    5: dict(name="cfg5 SU(4)AS 64x32^3", L=[64, 32, 32, 32], n=4, rep=3, mass=0.1, links="haar", tol=1e-10),
+}
+METRIC = "Dphi GFLOP/s and CG time-to-solution vs GPUs (1/2/4/8), % of HBM roofline"
+
+
+def decompose(L, n):
+    """T first while the local T stays >= 8 and even, then Z."""
+    grid = [1, 1, 1, 1]
+    left = n
+
+    def can_halve(d, floor):
+        loc = L[d] // (grid[d] * 2)
+        return left > 1 and left % 2 == 0 and L[d] % (grid[d] * 2) == 0 and loc % 2 == 0 and loc >= floor
+
+    while can_halve(0, 8):
+        grid[0] *= 2
+        left //= 2
+    for d in (3, 2, 1):
+        while can_halve(d, 2):
+            grid[d] *= 2
+            left //= 2
+    if left != 1:
+        raise SystemExit(f"cannot decompose {L} over {n} ranks")
+    return grid
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def bytes_full_dphi(dr, real):  # 128 d + 32 c d^2 per site
+    c = 1 if real else 2
+    return 128 * dr + 32 * c * dr * dr
+
+
+def bytes_eo_cg_iter(dr, real):  # per even site 4 B_hop + 11 * 64 d
+    c = 1 if real else 2
+    return 4 * (128 * dr + 64 * c * dr * dr) + 11 * 64 * dr
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampler run DURING the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device=0):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        try:
+            self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            self.reasons |= nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+            if not self.samples:
+                self._sample()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def traffic_from_profiles(key):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    import oracle as O
+
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference (its threads use every core)
+    L, n, rep = cfg["L"], cfg["n"], cfg["rep"]
+    dr = O.rep_dim(rep, n)
+    nthreads = os.cpu_count() or 1
+    grid = O.grid_for_threads(L, nthreads)
+    cores = int(np.prod(grid))
+    fps = O.ref_flops_per_site(O.DIRAC, dr, O.rep_is_real(rep))
+    V = int(np.prod(L))
+    # each step = one apply_dirac (bench.cpp:209) over the whole lattice
+    O.ref_bench_dirac(L, grid, n, rep, cfg["mass"], 1, max(1, args.warmup))
+    secs = O.ref_bench_dirac(L, grid, n, rep, cfg["mass"], 1, args.steps)
+    value = fps * V * args.steps / secs / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference keyed RNG, seed 1 (Haar links, Gaussian spinor)",
+        "config": {"workload": cfg["name"], "lattice": L, "group_rank": n, "rep": rep, "mass": cfg["mass"],
+                   "worker_grid": grid},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} apply_dirac on {cfg['name']}, {cores} worker threads"},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU arm
+def run_gpu(args, cfg):
+    import paper_1401_3733_b200 as lb
+
+    ws, rank, local = dist_env()
+    L, n, rep, mass = cfg["L"], cfg["n"], cfg["rep"], cfg["mass"]
+    grid = decompose(L, ws) if ws > 1 else [1, 1, 1, 1]
+    dist = None
+    world = None
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [lb.World.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        world = lb.World.nccl(ws, rank, obj[0])
+    dr = lb.rep_dim(rep, n)
+    real = lb.rep_is_real(rep)
+    links = {"haar": lb.LINKS_HAAR, "near_unit": lb.LINKS_NEAR_UNIT}[cfg["links"]]
+    ctx = lb.Context(L, grid, rank, local if ws > 1 else 0, world)
+    g = lb.init_gauge_random(L, n, rep, 1, grid=grid, rank=rank, links=links, eps=0.3)
+    s = lb.init_spinor_random(L, dr, 1, 0, grid=grid, rank=rank)
+    gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g)
+    del g
+    a = lb.SpinorField(ctx, dr).upload(s)
+    b = lb.SpinorField(ctx, dr)
+
+    def barrier():
+        ctx.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident Dphi ------------------------------------------------
+    for _ in range(args.warmup):
+        lb.apply_dirac(b, gauge, a, mass)
+    barrier()
+    l0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        barrier()
+        ctx.event_record(0)
+        for _ in range(args.steps):
+            lb.apply_dirac(b, gauge, a, mass)
+        ctx.event_record(1)
+        barrier()
+    launches = ctx.kernel_launches() - l0
+    ms = max_over_ranks(ctx.elapsed_ms(0, 1))
+    V = int(np.prod(L))
+    fps = lb.flops_per_site(lb.DIRAC, dr, real)
+    flops = fps * V * args.steps
+    value = flops / (ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    bpsite = bytes_full_dphi(dr, real)
+    per_launch_bytes = bpsite * V / ws  # one Dphi kernel per rank per step (N = 1: a single launch)
+    kernels_per_step = launches / args.steps
+    achieved = bpsite * V / ws / (ms * 1e-3 / args.steps) / 1e9
+
+    # ---- end to end through the C-ABI with host buffers ---------------------
+    import torch
+    nbytes = s.nbytes
+    hin = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    hout = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    hin.numpy()[:] = s.view(np.uint8).reshape(-1)
+    e2e_steps = max(1, min(args.steps, 20))
+    for _ in range(2):
+        a.upload_ptr(hin.data_ptr())
+        lb.apply_dirac(b, gauge, a, mass)
+        b.download_ptr(hout.data_ptr())
+    barrier()
+    t0 = time.perf_counter()
+    ctx.event_record(2)
+    for _ in range(e2e_steps):
+        a.upload_ptr(hin.data_ptr())
+        lb.apply_dirac(b, gauge, a, mass)
+        b.download_ptr(hout.data_ptr())
+    ctx.event_record(3)
+    barrier()
+    e2e_ms = max_over_ranks(ctx.elapsed_ms(2, 3))
+    e2e_value = fps * V * e2e_steps / (e2e_ms * 1e-3) / 1e9
+
+    # ---- CG time to solution (even-odd preconditioned, D^dag D) -------------
+    cg = None
+    if not args.no_cg:
+        rhs = lb.SpinorField(ctx, dr, lb.EVEN).upload(s)
+        st = lb.CgSettings(cfg["tol"], 20000)
+        lb.cg_solve_eo(gauge, mass, rhs, st)  # builds and caches the CUDA graph
+        barrier()
+        o = lb.cg_solve_eo(gauge, mass, rhs, st)
+        secs = max_over_ranks(o.seconds)
+        cg_bytes = (o.iterations * bytes_eo_cg_iter(dr, real) + 2 * (128 * dr + 64 * (1 if real else 2) * dr * dr)
+                    + 3 * 64 * dr) * V / 2
+        cg = {"solver": "eo CG on Mhat^dag Mhat", "tolerance": cfg["tol"], "iterations": o.iterations,
+              "seconds": secs, "true_rel_residual": o.true_rel_residual,
+              "hbm_frac": cg_bytes / secs / 1e9 / peak / ws}
+
+    # ---- CPU baseline (reference, rank 0 at N = 1, bounded sample) ----------
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        try:
+            import oracle as O
+            nthreads = os.cpu_count() or 1
+            cgrid = O.grid_for_threads(L, nthreads)
+            one = O.ref_bench_dirac(L, cgrid, n, rep, mass, 1, 1)
+            napps = int(max(1, min(200, args.cpu_seconds / max(one, 1e-6))))
+            secs = O.ref_bench_dirac(L, cgrid, n, rep, mass, 1, napps)
+            cpu = {"value": fps * V * napps / secs / 1e9, "unit": "GFLOP/s", "cores": int(np.prod(cgrid)),
+                   "kind": "reference",
+                   "sample": f"{napps} apply_dirac of the unmodified reference on {cfg['name']} "
+                             f"({int(np.prod(cgrid))} worker threads, grid {cgrid})"}
+        except Exception as e:  # the CPU baseline is reported, not required
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: reference keyed RNG, seed 1 (Haar / near-unit links, Gaussian spinor)",
+            "config": {"workload": cfg["name"], "lattice_TXYZ": L, "group_rank": n, "rep": rep, "dr": dr,
+                       "mass": mass, "bc": "periodic space, antiperiodic time", "grid": grid,
+                       "parallelism": f"domain decomposition {grid}",
+                       "l2": f"inputs larger than L2 ({(bpsite * V) / 1e6:.0f} MB touched per step vs 126 MB)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": per_launch_bytes,
+                         "kernel": "hop_kernel (full Dphi, both parities)",
+                         "kernels_per_step": kernels_per_step,
+                         "traffic": traffic_from_profiles(f"cfg{args.config}_dphi")},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": nbytes, "steps": e2e_steps},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cg": cg,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cg", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,409 @@
+// Streaming vector kernels, CG scalar kernels and host<->device layout
+// transposes (sm_100a).
+//
+// Replaces the reference's BLAS-1 helpers (proj/src/kernels.cpp:36-104,
+// proj/include/latbench/kernel_ops.hpp:105-121) and its global sums
+// (proj/src/transport.cpp:83-100): a spinor's parity blocks are one dense
+// double2 array (padding kept at zero), so every vector op is a flat,
+// coalesced grid-stride loop with 128-bit accesses; reductions are
+// deterministic (fixed-order block partials, see device.cuh).
+#include "objects.hpp"
+
+namespace lbcu {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+int flat_blocks(lbcu_ctx_s* ctx, size_t n) {
+  const size_t want = (n + kThreads * 4 - 1) / (kThreads * 4);
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>(want, ctx->max_partials)));
+}
+
+__global__ void k_sqnorm(const double2* __restrict__ a, size_t n, Reduce R) {
+  double v[1] = {0.0};
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 z = __ldg(a + i);
+    v[0] = fma(z.x, z.x, fma(z.y, z.y, v[0]));
+  }
+  block_reduce_finalize<1>(R, v);
+}
+
+// sum conj(a) b
+__global__ void k_dot(const double2* __restrict__ a, const double2* __restrict__ b, size_t n, Reduce R) {
+  double v[2] = {0.0, 0.0};
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 x = __ldg(a + i), y = __ldg(b + i);
+    v[0] = fma(x.x, y.x, fma(x.y, y.y, v[0]));
+    v[1] = fma(x.x, y.y, fma(-x.y, y.x, v[1]));
+  }
+  block_reduce_finalize<2>(R, v);
+}
+
+// y += a x
+__global__ void k_axpy(double2* __restrict__ y, const double2* __restrict__ x, size_t n, double ar, double ai) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 xv = __ldg(x + i);
+    double2 yv = y[i];
+    yv.x = fma(ar, xv.x, fma(-ai, xv.y, yv.x));
+    yv.y = fma(ar, xv.y, fma(ai, xv.x, yv.y));
+    y[i] = yv;
+  }
+}
+
+// y = x + a y
+__global__ void k_xpay(double2* __restrict__ y, const double2* __restrict__ x, size_t n, double ar, double ai) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 xv = __ldg(x + i);
+    const double2 yv = y[i];
+    y[i] = make_double2(fma(ar, yv.x, fma(-ai, yv.y, xv.x)), fma(ar, yv.y, fma(ai, yv.x, xv.y)));
+  }
+}
+
+// negate spin components 2,3 of every parity block: [2 dr stride, 4 dr stride)
+__global__ void k_gamma5(double2* __restrict__ f, size_t block_elems, size_t half, int nblocks) {
+  const size_t n = half * nblocks;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = i / half, j = i % half;
+    double2* p = f + b * block_elems + half + j;
+    const double2 v = *p;
+    *p = make_double2(-v.x, -v.y);
+  }
+}
+
+// ---- CG (device scalars in CgState) -------------------------------------
+// x += alpha p_old ; p = r + beta p_old      (deferred x update)
+__global__ void k_cg_p(double2* __restrict__ p, const double2* __restrict__ r, double2* __restrict__ x,
+                       size_t n, const CgState* __restrict__ st) {
+  const double alpha = st->alpha, beta = st->beta;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 pv = p[i], rv = __ldg(r + i);
+    double2 xv = x[i];
+    xv.x = fma(alpha, pv.x, xv.x);
+    xv.y = fma(alpha, pv.y, xv.y);
+    x[i] = xv;
+    p[i] = make_double2(fma(beta, pv.x, rv.x), fma(beta, pv.y, rv.y));
+  }
+}
+
+// r -= alpha ap ; |r|^2
+__global__ void k_cg_r(double2* __restrict__ r, const double2* __restrict__ ap, size_t n,
+                       const CgState* __restrict__ st, Reduce R) {
+  const double alpha = st->alpha;
+  double v[1] = {0.0};
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 a = __ldg(ap + i);
+    double2 rv = r[i];
+    rv.x = fma(-alpha, a.x, rv.x);
+    rv.y = fma(-alpha, a.y, rv.y);
+    r[i] = rv;
+    v[0] = fma(rv.x, rv.x, fma(rv.y, rv.y, v[0]));
+  }
+  block_reduce_finalize<1>(R, v);
+}
+
+__global__ void k_cg_xfinal(double2* __restrict__ x, const double2* __restrict__ p, size_t n,
+                            const CgState* __restrict__ st) {
+  const double alpha = st->alpha;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 pv = __ldg(p + i);
+    double2 xv = x[i];
+    xv.x = fma(alpha, pv.x, xv.x);
+    xv.y = fma(alpha, pv.y, xv.y);
+    x[i] = xv;
+  }
+}
+
+__global__ void k_cg_init(CgState* st, const double* b2, double tol, long long maxit) {
+  st->rr = *b2;
+  st->rr_new = *b2;
+  st->bnorm = sqrt(*b2);
+  st->tol = tol;
+  st->best = 1.0;
+  st->rel = 1.0;
+  st->alpha = 0.0;
+  st->beta = 0.0;
+  st->pap = 0.0;
+  st->k = 0;
+  st->maxit = maxit;
+  st->conv = 0;
+  st->done = 0;
+}
+
+__global__ void k_cg_alpha(CgState* st, const double* pap) {
+  st->pap = *pap;
+  st->alpha = st->rr / st->pap;
+}
+
+// end of iteration k (solver.cpp:58-69): relative residual, history,
+// convergence, beta, rr <- rr_new; optionally drives a graph while-loop.
+__global__ void k_cg_end(CgState* st, const double* rr_new, double* hist,
+                         cudaGraphConditionalHandle handle, int use_graph) {
+  const double rrn = *rr_new;
+  const double rel = sqrt(rrn) / st->bnorm;
+  const long long k = st->k;
+  hist[k] = rel;
+  st->rel = rel;
+  st->rr_new = rrn;
+  if (rel < st->best) st->best = rel;
+  st->k = k + 1;
+  if (rel < st->tol) {
+    st->conv = 1;
+    st->done = 1;
+  } else if (k + 1 >= st->maxit) {
+    st->done = 1;
+  }
+  st->beta = rrn / st->rr;
+  st->rr = rrn;
+  if (use_graph) cudaGraphSetConditional(handle, st->done ? 0u : 1u);
+}
+
+// ---- layout transposes -----------------------------------------------------
+__device__ __forceinline__ double neg(double a) { return -a; }
+__device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
+
+// Host order: site-major local lexicographic records of nv entries.
+// Device order: per parity block, entry-major [nv][stride] over cb sites.
+// A block stages TS consecutive sites (TS even -> TS/2 cb sites per parity).
+template <class T>
+__global__ void k_aos_to_soa(const T* __restrict__ src, T* dst0, T* dst1, int nv, long long vol,
+                             long long stride, int TS, DevGeo g, int sign_entries, int sign_t,
+                             int t_off) {
+  extern __shared__ unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const long long s0 = (long long)blockIdx.x * TS;
+  const int tile = TS * nv;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+    const long long gi = s0 * nv + e;
+    if (s0 + e / nv < vol) sm[e] = src[gi];
+  }
+  __syncthreads();
+  const int half = TS / 2;
+  for (int e = threadIdx.x; e < 2 * nv * half; e += blockDim.x) {
+    const int jj = e % half, k = (e / half) % nv, p = e / (half * nv);
+    T* dst = p ? dst1 : dst0;
+    if (!dst) continue;
+    const long long cb = s0 / 2 + jj;
+    if (2 * cb >= vol) continue;
+    int c[4], s;
+    cb_coords(g, (int)cb, p, c, s);
+    T v = sm[(s - s0) * nv + k];
+    if (k < sign_entries && c[0] + t_off == sign_t) v = neg(v);
+    dst[(long long)k * stride + cb] = v;
+  }
+}
+
+template <class T>
+__global__ void k_soa_to_aos(const T* src0, const T* src1, T* __restrict__ dst, int nv,
+                             long long vol, long long stride, int TS, DevGeo g) {
+  extern __shared__ unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const long long s0 = (long long)blockIdx.x * TS;
+  const int half = TS / 2;
+  for (int e = threadIdx.x; e < 2 * nv * half; e += blockDim.x) {
+    const int jj = e % half, k = (e / half) % nv, p = e / (half * nv);
+    const long long cb = s0 / 2 + jj;
+    if (2 * cb >= vol) continue;
+    int c[4], s;
+    cb_coords(g, (int)cb, p, c, s);
+    const T* src = p ? src1 : src0;
+    sm[(s - s0) * nv + k] = src ? src[(long long)k * stride + cb] : T{};
+  }
+  __syncthreads();
+  const int tile = TS * nv;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x)
+    if (s0 + e / nv < vol) dst[s0 * nv + e] = sm[e];
+}
+
+template <class T>
+int tile_sites(int nv) {
+  int ts = static_cast<int>((40 * 1024) / (nv * sizeof(T)));
+  ts = std::min(64, ts) & ~1;
+  return std::max(2, ts);
+}
+
+void ensure_staging(lbcu_ctx_s* ctx, size_t bytes) {
+  if (ctx->staging_bytes >= bytes) return;
+  if (ctx->staging) LBCU_CUDA(cudaFree(ctx->staging));
+  ctx->staging = nullptr;
+  LBCU_CUDA(cudaMalloc(&ctx->staging, bytes));
+  ctx->staging_bytes = bytes;
+}
+
+}  // namespace
+
+static Reduce make_reduce(lbcu_ctx_s* ctx, double* res, int blocks) {
+  return Reduce{ctx->partials, ctx->ticket, res, 0, blocks};
+}
+
+void blas_sqnorm(lbcu_ctx_s* ctx, const lbcu_spinor_s* f, double* dres) {
+  const int nb = flat_blocks(ctx, f->elems);
+  k_sqnorm<<<nb, kThreads, 0, ctx->stream>>>(f->base, f->elems, make_reduce(ctx, dres, nb));
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void blas_dot(lbcu_ctx_s* ctx, const lbcu_spinor_s* a, const lbcu_spinor_s* b, double* dres2) {
+  const int nb = flat_blocks(ctx, a->elems);
+  k_dot<<<nb, kThreads, 0, ctx->stream>>>(a->base, b->base, a->elems, make_reduce(ctx, dres2, nb));
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void blas_axpy(lbcu_ctx_s* ctx, lbcu_spinor_s* y, double ar, double ai, const lbcu_spinor_s* x) {
+  k_axpy<<<flat_blocks(ctx, y->elems), kThreads, 0, ctx->stream>>>(y->base, x->base, y->elems, ar, ai);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void blas_xpay(lbcu_ctx_s* ctx, lbcu_spinor_s* y, double ar, double ai, const lbcu_spinor_s* x) {
+  k_xpay<<<flat_blocks(ctx, y->elems), kThreads, 0, ctx->stream>>>(y->base, x->base, y->elems, ar, ai);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void blas_copy(lbcu_ctx_s* ctx, lbcu_spinor_s* dst, const lbcu_spinor_s* src) {
+  LBCU_CUDA(cudaMemcpyAsync(dst->base, src->base, dst->elems * sizeof(double2),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+void blas_zero(lbcu_ctx_s* ctx, lbcu_spinor_s* f) {
+  LBCU_CUDA(cudaMemsetAsync(f->base, 0, f->elems * sizeof(double2), ctx->stream));
+}
+
+void blas_gamma5(lbcu_ctx_s* ctx, lbcu_spinor_s* f) {
+  const size_t blk = static_cast<size_t>(4 * f->dr) * ctx->geo.stride;
+  const int nblocks = static_cast<int>(f->elems / blk);
+  const size_t half = blk / 2;
+  k_gamma5<<<flat_blocks(ctx, half * nblocks), kThreads, 0, ctx->stream>>>(f->base, blk, half, nblocks);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void cg_p_update(lbcu_ctx_s* ctx, lbcu_spinor_s* p, const lbcu_spinor_s* r, lbcu_spinor_s* x) {
+  k_cg_p<<<flat_blocks(ctx, p->elems), kThreads, 0, ctx->stream>>>(p->base, r->base, x->base, p->elems, ctx->dcg);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void cg_r_update(lbcu_ctx_s* ctx, lbcu_spinor_s* r, const lbcu_spinor_s* ap, double* dres) {
+  const int nb = flat_blocks(ctx, r->elems);
+  k_cg_r<<<nb, kThreads, 0, ctx->stream>>>(r->base, ap->base, r->elems, ctx->dcg, make_reduce(ctx, dres, nb));
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void cg_x_final(lbcu_ctx_s* ctx, lbcu_spinor_s* x, const lbcu_spinor_s* p) {
+  k_cg_xfinal<<<flat_blocks(ctx, x->elems), kThreads, 0, ctx->stream>>>(x->base, p->base, x->elems, ctx->dcg);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void cg_scalar_init(lbcu_ctx_s* ctx, const double* b2, double tol, long long maxit) {
+  k_cg_init<<<1, 1, 0, ctx->stream>>>(ctx->dcg, b2, tol, maxit);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void cg_scalar_alpha(lbcu_ctx_s* ctx, const double* pap) {
+  k_cg_alpha<<<1, 1, 0, ctx->stream>>>(ctx->dcg, pap);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void cg_scalar_end(lbcu_ctx_s* ctx, const double* rr_new, unsigned long long handle, int use_graph) {
+  k_cg_end<<<1, 1, 0, ctx->stream>>>(ctx->dcg, rr_new, ctx->dhist,
+                                     static_cast<cudaGraphConditionalHandle>(handle), use_graph);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+template <class T>
+static void launch_to_soa(lbcu_ctx_s* ctx, const T* src, T* d0, T* d1, int nv, int sign_entries) {
+  const Geometry& geo = ctx->geo;
+  const int TS = tile_sites<T>(nv);
+  const size_t smem = static_cast<size_t>(TS) * nv * sizeof(T);
+  const int blocks = static_cast<int>((geo.volume + TS - 1) / TS);
+  const int sign_t = sign_entries ? geo.global[0] - 1 : -1;
+  const int t_off = geo.coords[0] * geo.local[0];
+  k_aos_to_soa<T><<<blocks, 256, smem, ctx->stream>>>(src, d0, d1, nv, geo.volume, geo.stride, TS,
+                                                      ctx->dgeo, sign_entries, sign_t, t_off);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+template <class T>
+static void launch_to_aos(lbcu_ctx_s* ctx, const T* s0, const T* s1, T* dst, int nv) {
+  const Geometry& geo = ctx->geo;
+  const int TS = tile_sites<T>(nv);
+  const size_t smem = static_cast<size_t>(TS) * nv * sizeof(T);
+  const int blocks = static_cast<int>((geo.volume + TS - 1) / TS);
+  k_soa_to_aos<T><<<blocks, 256, smem, ctx->stream>>>(s0, s1, dst, nv, geo.volume, geo.stride, TS, ctx->dgeo);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void spinor_upload(lbcu_ctx_s* ctx, lbcu_spinor_s* s, const double* host) {
+  const int nv = 4 * s->dr;
+  const size_t bytes = static_cast<size_t>(ctx->geo.volume) * nv * sizeof(double2);
+  ensure_staging(ctx, bytes);
+  LBCU_CUDA(cudaMemcpyAsync(ctx->staging, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), s->par[0], s->par[1], nv, 0);
+  // value semantics: the caller may reuse its host buffer on return
+  LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void spinor_download(lbcu_ctx_s* ctx, const lbcu_spinor_s* s, double* host) {
+  const int nv = 4 * s->dr;
+  const size_t bytes = static_cast<size_t>(ctx->geo.volume) * nv * sizeof(double2);
+  ensure_staging(ctx, bytes);
+  launch_to_aos<double2>(ctx, s->par[0], s->par[1], static_cast<double2*>(ctx->staging), nv);
+  LBCU_CUDA(cudaMemcpyAsync(host, ctx->staging, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host) {
+  const int nv = 4 * g->dr * g->dr;
+  const size_t esz = g->real ? sizeof(double) : sizeof(double2);
+  const size_t bytes = static_cast<size_t>(ctx->geo.volume) * nv * esz;
+  ensure_staging(ctx, bytes);
+  LBCU_CUDA(cudaMemcpyAsync(ctx->staging, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const int sign = g->bc == LBCU_BC_ANTIPERIODIC_T ? g->dr * g->dr : 0;
+  const size_t pstride = static_cast<size_t>(nv) * ctx->geo.stride;
+  if (g->real) {
+    double* b = static_cast<double*>(g->base);
+    launch_to_soa<double>(ctx, static_cast<const double*>(ctx->staging), b, b + pstride, nv, sign);
+  } else {
+    double2* b = static_cast<double2*>(g->base);
+    launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b, b + pstride, nv, sign);
+  }
+  // the staging buffer is reused by the next transfer: finish this one first
+  LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host) {
+  const int nv = 4 * g->dr * g->dr;
+  const size_t esz = g->real ? sizeof(double) : sizeof(double2);
+  const size_t bytes = static_cast<size_t>(ctx->geo.volume) * nv * esz;
+  ensure_staging(ctx, bytes);
+  const size_t pstride = static_cast<size_t>(nv) * ctx->geo.stride;
+  if (g->real) {
+    const double* b = static_cast<const double*>(g->base);
+    launch_to_aos<double>(ctx, b, b + pstride, static_cast<double*>(ctx->staging), nv);
+  } else {
+    const double2* b = static_cast<const double2*>(g->base);
+    launch_to_aos<double2>(ctx, b, b + pstride, static_cast<double2*>(ctx->staging), nv);
+  }
+  LBCU_CUDA(cudaMemcpyAsync(host, ctx->staging, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (g->bc == LBCU_BC_ANTIPERIODIC_T) {  // report the links as uploaded (undo the BC sign)
+    const Geometry& geo = ctx->geo;
+    const int per = nv * (g->real ? 1 : 2);
+    const int64_t slab = geo.volume / geo.local[0];
+    if (geo.coords[0] == geo.grid[0] - 1)
+      for (int64_t s = (geo.local[0] - 1) * slab; s < geo.volume; ++s)
+        for (int k = 0; k < g->dr * g->dr * (g->real ? 1 : 2); ++k) host[s * per + k] = -host[s * per + k];
+  }
+}
+
+}  // namespace lbcu

@@ -1,0 +1,177 @@
+// Device-side building blocks shared by the kernels: even-odd indexing,
+// the gamma-basis spin tables, unit-phase arithmetic and deterministic
+// block reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lbcu {
+
+// Local lattice as seen by a kernel. Sites of one parity are stored in
+// "checkerboard" order cb = s >> 1 of the local lexicographic index s
+// (t,x,y,z; z fastest). Every local extent is even, so (z, z+1) pairs split
+// across parities and each parity block is dense.
+struct DevGeo {
+  int L[4];       // local extents t, x, y, z
+  int sx[4];      // lexicographic strides: Lx*Ly*Lz, Ly*Lz, Lz, 1
+  int vh;         // sites per parity
+  long long stride;  // component stride of one parity block (>= vh)
+  int wrap[4];    // 1: direction not decomposed -> local periodic wrap
+};
+
+// cb index + parity -> local coordinates and lexicographic index
+__device__ __forceinline__ void cb_coords(const DevGeo& g, int i, int par, int c[4], int& s) {
+  const int s0 = 2 * i;
+  const int z0 = s0 % g.L[3];
+  int r = s0 / g.L[3];
+  c[2] = r % g.L[2];
+  r /= g.L[2];
+  c[1] = r % g.L[1];
+  c[0] = r / g.L[1];
+  const int dz = (c[0] + c[1] + c[2] + z0 + par) & 1;
+  c[3] = z0 + dz;
+  s = s0 + dz;
+}
+
+// lexicographic neighbour of s in direction mu (periodic inside the rank)
+__device__ __forceinline__ int nb_fwd(const DevGeo& g, int s, const int c[4], int mu) {
+  return (c[mu] + 1 < g.L[mu]) ? s + g.sx[mu] : s - (g.L[mu] - 1) * g.sx[mu];
+}
+__device__ __forceinline__ int nb_bwd(const DevGeo& g, int s, const int c[4], int mu) {
+  return (c[mu] > 0) ? s - g.sx[mu] : s + (g.L[mu] - 1) * g.sx[mu];
+}
+
+// in-face lexicographic position over the three coordinates other than mu
+__device__ __forceinline__ int face_pos(const DevGeo& g, const int c[4], int mu) {
+  int p = 0;
+#pragma unroll
+  for (int d = 0; d < 4; ++d)
+    if (d != mu) p = p * g.L[d] + c[d];
+  return p;
+}
+
+// ---- gamma basis (proj/src/gamma.cpp:46-61, chiral, gamma5 = diag(1,1,-1,-1)).
+// Unit phases P1, M1, PI, MI as 0..3 (proj/include/latbench/gamma.hpp:18);
+// negation flips the low bit. (1 - gamma_mu) psi projects to
+//   h_a = psi_a + PROJ_PH[mu][a] psi_{PAIR[mu][a]}, a = 0, 1
+// and reconstructs as (h0, h1, REC_PH[mu][0] h_{REC[mu][0]}, REC_PH[mu][1] h_{REC[mu][1]}).
+// (1 + gamma_mu) uses the same pairs with negated phases.
+template <int MU>
+struct Gam;
+template <>
+struct Gam<0> {
+  static constexpr int p0 = 2, p1 = 3, f0 = 0, f1 = 0, r0 = 0, r1 = 1, q0 = 0, q1 = 0;
+};
+template <>
+struct Gam<1> {
+  static constexpr int p0 = 3, p1 = 2, f0 = 2, f1 = 2, r0 = 1, r1 = 0, q0 = 3, q1 = 3;
+};
+template <>
+struct Gam<2> {
+  static constexpr int p0 = 3, p1 = 2, f0 = 0, f1 = 1, r0 = 1, r1 = 0, q0 = 1, q1 = 0;
+};
+template <>
+struct Gam<3> {
+  static constexpr int p0 = 2, p1 = 3, f0 = 2, f1 = 3, r0 = 0, r1 = 1, q0 = 3, q1 = 2;
+};
+
+template <int P>
+__device__ __forceinline__ double2 phm(double2 z) {
+  if constexpr (P == 0) return z;
+  else if constexpr (P == 1) return make_double2(-z.x, -z.y);
+  else if constexpr (P == 2) return make_double2(-z.y, z.x);
+  else return make_double2(z.y, -z.x);
+}
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+
+// acc += u * v
+__device__ __forceinline__ void cmac(double2& acc, double2 u, double2 v) {
+  acc.x = fma(u.x, v.x, fma(-u.y, v.y, acc.x));
+  acc.y = fma(u.x, v.y, fma(u.y, v.x, acc.y));
+}
+// acc += conj(u) * v
+__device__ __forceinline__ void cmac_conj(double2& acc, double2 u, double2 v) {
+  acc.x = fma(u.x, v.x, fma(u.y, v.y, acc.x));
+  acc.y = fma(u.x, v.y, fma(-u.y, v.x, acc.y));
+}
+// acc += r * v (real link)
+__device__ __forceinline__ void rmac(double2& acc, double u, double2 v) {
+  acc.x = fma(u, v.x, acc.x);
+  acc.y = fma(u, v.y, acc.y);
+}
+
+template <class T>
+__device__ __forceinline__ T ldg(const T* p) {
+  return __ldg(p);
+}
+
+// ---- deterministic reductions ---------------------------------------------
+// Each block reduces NR values (warp shuffles + shared memory) and writes its
+// partials to part[(offset + blockIdx) * NR + k]. The block that arrives last
+// on the ticket sums all partials in a fixed order and writes result[k], so
+// the value does not depend on block scheduling.
+struct Reduce {
+  double* part;        // partials, >= total_blocks * NR
+  unsigned* ticket;    // zero between reductions
+  double* result;      // NR outputs
+  int offset;          // this launch's first partial slot
+  int total_blocks;    // partial slots over all launches that feed this result
+};
+
+template <int NR>
+__device__ __forceinline__ void block_reduce_finalize(const Reduce& R, double (&v)[NR]) {
+  __shared__ double sh[32][NR];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < NR; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) sh[warp][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      s[k] = 0.0;
+      for (int w = 0; w < nwarps; ++w) s[k] += sh[w][k];
+      R.part[(size_t)(R.offset + blockIdx.x) * NR + k] = s[k];
+    }
+    __threadfence();
+    const unsigned t = atomicAdd(R.ticket, 1u);
+    last = (t == (unsigned)R.total_blocks - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) acc[k] = 0.0;
+  for (int b = threadIdx.x; b < R.total_blocks; b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) acc[k] += __ldcg(&R.part[(size_t)b * NR + k]);
+#pragma unroll
+  for (int k = 0; k < NR; ++k)
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], o);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) sh[warp][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < nwarps; ++w) s += sh[w][k];
+      R.result[k] = s;
+    }
+    *R.ticket = 0u;
+  }
+}
+
+}  // namespace lbcu

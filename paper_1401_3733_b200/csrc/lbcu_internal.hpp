@@ -1,0 +1,98 @@
+// Internal host-side types of the latbench-b200 library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lbcu.h"
+
+namespace lbcu {
+
+// Status-carrying exception; every C-ABI entry point converts it to a code.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define LBCU_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::lbcu::Error(LBCU_CUDA_ERROR, std::string(#call " failed: ") +               \
+                                               cudaGetErrorString(e_) + " at " __FILE__); \
+  } while (0)
+
+int rep_dim(int rep, int n);  // group.cpp:29-38
+
+// One rank's view of the decomposed lattice (proj/src/geometry.cpp:70-130),
+// plus the even-odd device indexing.
+struct Geometry {
+  int global[4]{}, grid[4]{}, local[4]{}, coords[4]{};
+  int rank = 0, nranks = 1;
+  int64_t volume = 0;  // local interior sites
+  int64_t vh = 0;      // sites per parity
+  int64_t stride = 0;  // padded component stride (elements) of one parity block
+  bool decomposed[4]{};
+  bool any_decomposed = false;
+
+  void global_coords(int64_t s, int* gc) const {
+    int lc[4];
+    int64_t r = s;
+    for (int d = 3; d >= 0; --d) {
+      lc[d] = static_cast<int>(r % local[d]);
+      r /= local[d];
+    }
+    for (int d = 0; d < 4; ++d) gc[d] = coords[d] * local[d] + lc[d];
+  }
+};
+
+Geometry build_geometry(const int global[4], const int grid[4], int rank, bool enforce_floor);
+
+void host_spinor_random(const Geometry& geo, int dr, uint64_t seed, uint64_t field, double* out);
+void host_gauge_random(const Geometry& geo, int n, int rep, int links, uint64_t seed, double eps,
+                       int nthreads, double* out);
+
+// Face schedule for the even-odd halo exchange (see lbcu_plan_faces).
+struct FacePlan {
+  int partner[8]{};   // f = 2 mu + dir; dir 0 -> -mu partner, dir 1 -> +mu partner
+  int64_t count[8]{}; // records per message (half the face)
+};
+FacePlan plan_faces(const Geometry& geo);
+// local lexicographic site of record j on face f for the given input parity
+int64_t face_site(const Geometry& geo, int f, int input_parity, int64_t j);
+
+// ---------------------------------------------------------------- transport
+struct Transport {
+  virtual ~Transport() = default;
+  virtual int nranks() const = 0;
+  virtual bool capturable() const = 0;  // may be recorded into a CUDA graph
+  // in-place sum of n doubles in device memory across ranks, stream-ordered
+  virtual void allreduce(int rank, double* dev, int n, cudaStream_t s) = 0;
+  // exchange: for each message i, send send[i] (bytes[i]) to peer_send[i] and
+  // receive recv[i] (bytes[i]) from peer_recv[i]; stream-ordered.
+  struct Msg {
+    const void* send;
+    void* recv;
+    size_t bytes;
+    int peer_send, peer_recv;
+  };
+  virtual void exchange(int rank, const std::vector<Msg>& msgs, cudaStream_t s) = 0;
+  virtual void barrier(int rank) = 0;
+};
+
+std::unique_ptr<Transport> make_single_transport();
+std::unique_ptr<Transport> make_thread_transport(int nranks);
+std::unique_ptr<Transport> make_nccl_transport(int nranks, int rank, const unsigned char id[128]);
+void nccl_unique_id(unsigned char id[128]);
+
+}  // namespace lbcu
+
+struct lbcu_world_s {
+  std::unique_ptr<lbcu::Transport> t;
+};

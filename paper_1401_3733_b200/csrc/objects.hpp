@@ -1,0 +1,129 @@
+// Library objects behind the opaque C-ABI handles, and the launcher entry
+// points the .cu translation units provide.
+#pragma once
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "device.cuh"
+#include "lbcu_internal.hpp"
+
+struct lbcu_ctx_s;
+
+struct lbcu_spinor_s {
+  lbcu_ctx_s* ctx = nullptr;
+  int dr = 0;
+  int subset = LBCU_FULL;
+  double2* base = nullptr;
+  double2* par[2] = {nullptr, nullptr};  // parity blocks [4 dr][stride]
+  size_t elems = 0;                      // double2 elements over present parities
+  bool has(int p) const { return par[p] != nullptr; }
+};
+
+struct lbcu_gauge_s {
+  lbcu_ctx_s* ctx = nullptr;
+  int n = 0, rep = 0, dr = 0, bc = 0;
+  bool real = false;
+  void* base = nullptr;  // [2 parity][4 mu][dr][dr][stride] of double2 (complex) or double
+  size_t bytes = 0;
+};
+
+namespace lbcu {
+
+enum Epi { EPI_STORE = 0, EPI_STORE_NORM = 1, EPI_CG = 2 };
+
+// Device CG state (one per context), see cg.cu.
+struct CgState {
+  double rr, rr_new, pap, alpha, beta, bnorm, tol, best, rel;
+  long long k, maxit;
+  int conv, done;
+};
+
+struct HaloBufs {
+  double2* send[8] = {};
+  double2* recv[8] = {};
+  size_t cap = 0;  // double2 per buffer
+};
+
+}  // namespace lbcu
+
+struct lbcu_ctx_s {
+  lbcu_world_s* world = nullptr;
+  bool owns_world = false;
+  int rank = 0, device = 0;
+  lbcu::Geometry geo;
+  lbcu::FacePlan plan;
+  lbcu::DevGeo dgeo{};
+  cudaStream_t stream = nullptr;
+  cudaStream_t comm_stream = nullptr;  // halo exchange (decomposed runs)
+  cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
+  cudaEvent_t ev[16] = {};
+  // reduction workspace
+  double* partials = nullptr;
+  int max_partials = 0;
+  unsigned* ticket = nullptr;
+  double* dscal = nullptr;  // 64 device scalars (reduction results)
+  double* hscal = nullptr;  // pinned mirror
+  // interior / boundary site lists per output parity (decomposed runs only)
+  int* ilist[2] = {nullptr, nullptr};
+  int* blist[2] = {nullptr, nullptr};
+  int nint[2] = {0, 0}, nbnd[2] = {0, 0};
+  std::map<int, lbcu::HaloBufs> halo;  // keyed by dr
+  std::map<std::tuple<int, int, int>, lbcu_spinor_s*> scratch;  // (dr, subset, slot)
+  lbcu::CgState* dcg = nullptr;
+  lbcu::CgState* hcg = nullptr;  // pinned
+  double* dhist = nullptr;
+  long long hist_cap = 0;
+  void* staging = nullptr;  // device staging buffer for host<->device layout transposes
+  size_t staging_bytes = 0;
+  long long launches = 0;
+};
+
+namespace lbcu {
+
+// ---- launchers (stream-ordered on ctx->stream) --------------------------
+struct HopCall {
+  const lbcu_spinor_s* in = nullptr;
+  lbcu_spinor_s* out = nullptr;
+  const lbcu_spinor_s* x = nullptr;  // diagonal term (same parity set as out)
+  lbcu_spinor_s* r = nullptr;        // EPI_CG residual
+  const lbcu_gauge_s* g = nullptr;
+  int out_parity = 2;  // 0 even, 1 odd, 2 both
+  double a = 0.0, b = 1.0;
+  double s5in = 1.0, s5x = 1.0, s5acc = 1.0;
+  int epi = EPI_STORE;
+  const double* alpha = nullptr;  // EPI_CG scalar (device)
+  double* result = nullptr;       // reduction output (device), EPI != STORE
+};
+void hop_apply(lbcu_ctx_s* ctx, const HopCall& c);
+
+// flat BLAS over the present parity blocks (padding included, kept at zero)
+void blas_sqnorm(lbcu_ctx_s* ctx, const lbcu_spinor_s* f, double* dres);
+void blas_dot(lbcu_ctx_s* ctx, const lbcu_spinor_s* a, const lbcu_spinor_s* b, double* dres2);
+void blas_axpy(lbcu_ctx_s* ctx, lbcu_spinor_s* y, double are, double aim, const lbcu_spinor_s* x);
+void blas_xpay(lbcu_ctx_s* ctx, lbcu_spinor_s* y, double are, double aim, const lbcu_spinor_s* x);
+void blas_copy(lbcu_ctx_s* ctx, lbcu_spinor_s* dst, const lbcu_spinor_s* src);
+void blas_zero(lbcu_ctx_s* ctx, lbcu_spinor_s* f);
+void blas_gamma5(lbcu_ctx_s* ctx, lbcu_spinor_s* f);
+// CG helpers reading scalars from the device CgState
+void cg_p_update(lbcu_ctx_s* ctx, lbcu_spinor_s* p, const lbcu_spinor_s* r, lbcu_spinor_s* x);
+void cg_r_update(lbcu_ctx_s* ctx, lbcu_spinor_s* r, const lbcu_spinor_s* ap, double* dres);
+void cg_x_final(lbcu_ctx_s* ctx, lbcu_spinor_s* x, const lbcu_spinor_s* p);
+void cg_scalar_alpha(lbcu_ctx_s* ctx, const double* pap);
+void cg_scalar_end(lbcu_ctx_s* ctx, const double* rr_new, unsigned long long graph_handle,
+                   int use_graph);
+void cg_scalar_init(lbcu_ctx_s* ctx, const double* b2, double tol, long long maxit);
+
+// layout transposes host (reference AoS) <-> device (even-odd SoA)
+void spinor_upload(lbcu_ctx_s* ctx, lbcu_spinor_s* s, const double* host);
+void spinor_download(lbcu_ctx_s* ctx, const lbcu_spinor_s* s, double* host);
+void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host);
+void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host);
+
+// helpers in api.cpp
+lbcu_spinor_s* scratch_spinor(lbcu_ctx_s* ctx, int dr, int subset, int slot);
+void reduce_slot_reset(lbcu_ctx_s* ctx);
+int reduce_blocks_cap(lbcu_ctx_s* ctx);
+
+}  // namespace lbcu

@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle.
+
+Bar (BASELINE.json north_star): Dphi within 1e-12 relative L2 per field in
+fp64; CG iterations within +-1 of the reference with the true residual below
+the tolerance. Inputs are the reference's own seeded generators (seed 1).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1401_3733_b200 as lb
+from helpers import REP_IDS, REPS, global_index, rel_l2, run_ranks
+
+pytestmark = pytest.mark.gpu
+
+TOL_DPHI = 1e-12  # relative L2, north_star
+
+
+def fields(L, n, rep, seed=1, field=0, links=lb.LINKS_HAAR):
+    dr = lb.rep_dim(rep, n)
+    g = lb.init_gauge_random(L, n, rep, seed, links=links)
+    s = lb.init_spinor_random(L, dr, seed, field)
+    return dr, g, s
+
+
+def setup(L, n, rep, bc=lb.ANTIPERIODIC_T, grid=(1, 1, 1, 1)):
+    ctx = lb.Context(L, grid)
+    dr, g, s = fields(L, n, rep)
+    gauge = lb.GaugeField(ctx, n, rep, bc).upload(g)
+    return ctx, dr, g, s, gauge
+
+
+@pytest.mark.parametrize("n,rep", REPS, ids=REP_IDS)
+@pytest.mark.parametrize("bc", [lb.PERIODIC, lb.ANTIPERIODIC_T], ids=["periodic", "antiperiodic"])
+def test_dphi_matches_oracle(n, rep, bc):
+    L = [8, 4, 4, 6]
+    ctx, dr, g, s, gauge = setup(L, n, rep, bc)
+    inp = lb.SpinorField(ctx, dr).upload(s)
+    out = lb.SpinorField(ctx, dr)
+    lb.apply_dirac(out, gauge, inp, 0.1)
+    got = out.download()
+    want = O.port_dirac(L, bc, 0.1, g, s)
+    assert rel_l2(got, want) < TOL_DPHI
+    # and the unmodified reference itself
+    ref = O.ref_apply_dirac(L, [1, 1, 1, 1], n, rep, bc, 0.1, g, s)
+    assert rel_l2(got, ref) < TOL_DPHI
+
+
+@pytest.mark.parametrize("n,rep", REPS, ids=REP_IDS)
+def test_g5dphi_and_h(n, rep):
+    L = [4, 4, 6, 4]
+    ctx, dr, g, s, gauge = setup(L, n, rep)
+    inp = lb.SpinorField(ctx, dr).upload(s)
+    out = lb.SpinorField(ctx, dr)
+    lb.apply_g5dirac(out, gauge, inp, 0.05)
+    want = O.port_dirac(L, 1, 0.05, g, s)
+    want[:, 2:, :] *= -1
+    assert rel_l2(out.download(), want) < TOL_DPHI
+    lb.apply_h(out, gauge, inp, 0.05)
+    ref = O.ref_apply_h(L, [1, 1, 1, 1], n, rep, 1, 0.05, g, s)
+    assert rel_l2(out.download(), ref) < TOL_DPHI
+
+
+@pytest.mark.parametrize("n,rep", REPS, ids=REP_IDS)
+def test_eo_blocks_and_mhat(n, rep):
+    L = [4, 6, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, n, rep)
+    even = O.parity_mask(L)
+    e_in = lb.SpinorField(ctx, dr, lb.EVEN).upload(s)
+    o_in = lb.SpinorField(ctx, dr, lb.ODD).upload(s)
+    e_out = lb.SpinorField(ctx, dr, lb.EVEN)
+    o_out = lb.SpinorField(ctx, dr, lb.ODD)
+    lb.dphi_eo(e_out, gauge, o_in)
+    s_odd = s.copy()
+    s_odd[even] = 0
+    want = O.port_hop_parity(L, 1, 0, -0.5, g, s_odd)
+    assert rel_l2(e_out.download(), want) < TOL_DPHI
+    lb.dphi_oe(o_out, gauge, e_in)
+    s_even = s.copy()
+    s_even[~even] = 0
+    want = O.port_hop_parity(L, 1, 1, -0.5, g, s_even)
+    assert rel_l2(o_out.download(), want) < TOL_DPHI
+    lb.mhat(e_out, gauge, e_in, 0.1)
+    got = e_out.download()
+    assert rel_l2(got, O.port_mhat(L, 1, 0.1, g, s)) < TOL_DPHI
+    assert rel_l2(got, O.ref_mhat(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s)) < TOL_DPHI
+
+
+def test_unit_gauge_constant_spinor_mass_identity():
+    """unit links, constant spinor, periodic BC -> D psi = m psi."""
+    L = [4, 4, 4, 4]
+    ctx = lb.Context(L)
+    gauge = lb.GaugeField(ctx, 3, lb.FUNDAMENTAL, lb.PERIODIC)
+    gauge.upload(lb.init_gauge_random(L, 3, lb.FUNDAMENTAL, 1, links=lb.LINKS_UNIT))
+    rng = np.random.default_rng(0)
+    site = rng.normal(size=(4, 3)) + 1j * rng.normal(size=(4, 3))
+    s = np.broadcast_to(site, (256, 4, 3)).copy()
+    inp = lb.SpinorField(ctx, 3).upload(s)
+    out = lb.SpinorField(ctx, 3)
+    lb.apply_dirac(out, gauge, inp, 0.37)
+    assert np.abs(out.download() - 0.37 * s).max() < 1e-13
+
+
+@pytest.mark.parametrize("n,rep", REPS[:2], ids=REP_IDS[:2])
+def test_blas_matches_reference(n, rep):
+    L = [4, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, n, rep)
+    s1 = lb.init_spinor_random(L, dr, 1, 1)
+    a = lb.SpinorField(ctx, dr).upload(s)
+    b = lb.SpinorField(ctx, dr).upload(s1)
+    assert abs(lb.sqnorm(a) - O.ref_sqnorm(L, [1, 1, 1, 1], s)) < 1e-10 * O.ref_sqnorm(L, [1, 1, 1, 1], s)
+    d = lb.dot(a, b)
+    dr_ = O.ref_dot(L, [1, 1, 1, 1], s, s1)
+    assert abs(d - dr_) < 1e-10 * abs(dr_) + 1e-9
+    lb.mul_add(a, 0.3 + 0.7j, b)
+    assert rel_l2(a.download(), O.ref_mul_add(L, [1, 1, 1, 1], 0.3 + 0.7j, s, s1)) < 1e-15
+    lb.apply_gamma5(b)
+    w = s1.copy()
+    w[:, 2:] *= -1
+    assert np.array_equal(b.download(), w)
+
+
+@pytest.mark.parametrize("n,rep", REPS, ids=REP_IDS)
+def test_cg_h_matches_reference(n, rep):
+    L = [8, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, n, rep)
+    rhs = lb.SpinorField(ctx, dr).upload(s)
+    st = lb.CgSettings(1e-10, 1000)
+    o = lb.cg_solve_h(gauge, 0.1, rhs, st)
+    ref = O.ref_cg_h(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s, 1e-10)
+    assert abs(o.iterations - ref["iterations"]) <= 1
+    assert o.true_rel_residual < 2e-10
+    assert rel_l2(o.solution.download(), ref["x"]) < 1e-8
+    assert len(o.residual_history) == o.iterations
+
+
+@pytest.mark.parametrize("n,rep", REPS, ids=REP_IDS)
+def test_cg_eo_matches_oracle(n, rep):
+    L = [8, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, n, rep)
+    rhs = lb.SpinorField(ctx, dr, lb.EVEN).upload(s)
+    o = lb.cg_solve_eo(gauge, 0.1, rhs, lb.CgSettings(1e-10, 1000))
+    ref = O.ref_cg_eo(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s, 1e-10)
+    assert abs(o.iterations - ref["iterations"]) <= 1
+    assert o.true_rel_residual < 2e-10
+    x = o.solution.download()
+    assert rel_l2(x, ref["x"]) < 1e-8
+
+
+def test_cg_callback_operator_matches_fused():
+    L = [8, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, 3, lb.FUNDAMENTAL)
+    rhs = lb.SpinorField(ctx, dr).upload(s)
+    tmp = lb.SpinorField(ctx, dr)
+    calls = []
+
+    def op(out, inp):  # make_h_operator composed from the public kernels (solver.cpp:9-15)
+        calls.append(1)
+        lb.apply_dirac(tmp, gauge, inp, 0.1)
+        lb.apply_gamma5(tmp)
+        lb.apply_dirac(out, gauge, tmp, 0.1)
+        lb.apply_gamma5(out)
+
+    o = lb.cg_solve(op, rhs, lb.CgSettings(1e-10, 500))
+    f = lb.cg_solve_h(gauge, 0.1, rhs, lb.CgSettings(1e-10, 500))
+    assert abs(o.iterations - f.iterations) <= 1
+    assert len(calls) == o.iterations + 1  # + the true-residual application
+    assert rel_l2(o.solution.download(), f.solution.download()) < 1e-8
+
+
+def test_cg_zero_rhs_and_nonconvergence():
+    L = [4, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, 3, lb.FUNDAMENTAL)
+    z = lb.SpinorField(ctx, dr)
+    o = lb.cg_solve_h(gauge, 0.1, z)
+    assert o.iterations == 0 and not np.any(o.solution.download())
+    rhs = lb.SpinorField(ctx, dr).upload(s)
+    with pytest.raises(lb.NonConvergence) as ei:
+        lb.cg_solve_h(gauge, 0.1, rhs, lb.CgSettings(1e-12, 3))
+    assert ei.value.iterations == 3 and 0 < ei.value.best_residual < 1
+
+
+def test_planted_solution_recovered():
+    """rhs = H x0 -> x0 recovered to 1e-5 at tol 1e-7."""
+    L = [4, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, 2, lb.FUNDAMENTAL)
+    x0 = lb.SpinorField(ctx, dr).upload(s)
+    rhs = lb.SpinorField(ctx, dr)
+    lb.apply_h(rhs, gauge, x0, 0.1)
+    o = lb.cg_solve_h(gauge, 0.1, rhs, lb.CgSettings(1e-7))
+    assert rel_l2(o.solution.download(), s) < 1e-5
+
+
+def test_tampered_operator_fails_consistency():
+    """a sign-flipped Dirac operator must fail the true-residual check."""
+    L = [4, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, 3, lb.FUNDAMENTAL)
+    rhs = lb.SpinorField(ctx, dr).upload(s)
+    tmp = lb.SpinorField(ctx, dr)
+    state = {"n": 0}
+
+    def op(out, inp):
+        state["n"] += 1
+        lb.apply_h(out, gauge, inp, 0.1)
+        if state["n"] % 2 == 0:  # corrupt every second application
+            lb.axpy(out, -1e-3, inp)
+
+    try:
+        o = lb.cg_solve(op, rhs, lb.CgSettings(1e-10, 300))
+        assert o.true_rel_residual >= 2e-10
+    except lb.NonConvergence:
+        pass
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1, 1), (2, 1, 1, 2), (1, 2, 2, 1)], ids=["t2", "t2z2", "x2y2"])
+@pytest.mark.parametrize("n,rep", [REPS[0], REPS[3]], ids=[REP_IDS[0], REP_IDS[3]])
+def test_decomposed_dphi_matches_single(grid, n, rep):
+    """Serial oracle vs decomposition: ranks as host threads on one GPU,
+    half-spinor halos packed by kernels and exchanged by the thread transport."""
+    L = [8, 4, 4, 8]
+    dr, g, s = fields(L, n, rep)
+    want = O.port_dirac(L, 1, 0.1, g, s)
+    nranks = int(np.prod(grid))
+    world = lb.World.threads(nranks)
+
+    def body(r):
+        ctx = lb.Context(L, grid, r, 0, world)
+        idx = global_index(L, grid, r)
+        gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g[idx])
+        inp = lb.SpinorField(ctx, dr).upload(s[idx])
+        out = lb.SpinorField(ctx, dr)
+        lb.apply_dirac(out, gauge, inp, 0.1)
+        return idx, out.download()
+
+    got = np.empty_like(want)
+    for idx, part in run_ranks(nranks, body):
+        got[idx] = part
+    assert rel_l2(got, want) < 1e-14
+
+
+def test_decomposed_cg_eo_matches_single():
+    L = [8, 4, 4, 8]
+    n, rep = 3, lb.FUNDAMENTAL
+    dr, g, s = fields(L, n, rep)
+    ref = O.ref_cg_eo(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s, 1e-10)
+    grid = (2, 1, 1, 2)
+    world = lb.World.threads(4)
+
+    def body(r):
+        ctx = lb.Context(L, grid, r, 0, world)
+        idx = global_index(L, grid, r)
+        gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g[idx])
+        rhs = lb.SpinorField(ctx, dr, lb.EVEN).upload(s[idx])
+        o = lb.cg_solve_eo(gauge, 0.1, rhs, lb.CgSettings(1e-10, 500))
+        return idx, o.iterations, o.true_rel_residual, o.solution.download()
+
+    x = np.empty_like(s)
+    for idx, it, tr, part in run_ranks(4, body):
+        assert abs(it - ref["iterations"]) <= 1
+        assert tr < 2e-10
+        x[idx] = part
+    assert rel_l2(x, ref["x"]) < 1e-8
+
+
+def test_near_unit_links_cg_eo():
+    """BASELINE config 3 structure (near-unit links, small mass) at a reduced volume."""
+    L = [8, 4, 4, 4]
+    n, rep = 3, lb.FUNDAMENTAL
+    dr, g, s = fields(L, n, rep, links=lb.LINKS_NEAR_UNIT)
+    ctx = lb.Context(L)
+    gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g)
+    rhs = lb.SpinorField(ctx, dr, lb.EVEN).upload(s)
+    o = lb.cg_solve_eo(gauge, 0.02, rhs, lb.CgSettings(1e-12, 2000))
+    ref = O.ref_cg_eo(L, [1, 1, 1, 1], n, rep, 1, 0.02, g, s, 1e-12)
+    assert abs(o.iterations - ref["iterations"]) <= 1
+    assert o.true_rel_residual < 2e-12
