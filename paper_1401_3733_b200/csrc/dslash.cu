@@ -22,6 +22,7 @@
 //   face dir 0 (to -mu partner): h = (1 - g_mu) projection of in at x_mu = 0
 //   face dir 1 (to +mu partner): g = U_mu(y)^dag (1 + g_mu) projection at
 //                                x_mu = L_mu - 1 (no gauge halo needed).
+#include <cstdlib>
 #include <type_traits>
 
 #include "objects.hpp"
@@ -152,8 +153,8 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
   }
 }
 
-template <int D, bool REAL, bool BND, int EPI>
-__global__ void __launch_bounds__(128) hop_kernel(const __grid_constant__ HopArgs A) {
+template <int D, bool REAL, bool BND, int EPI, int MINB>
+__global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ HopArgs A) {
   int par, idx;
   if (A.both) {
     par = blockIdx.x & 1;
@@ -280,12 +281,31 @@ __global__ void __launch_bounds__(128) pack_kernel(const __grid_constant__ PackA
 
 constexpr int kBlock = 128;
 
+// Occupancy knob: LBCU_HOP_MINB = minimum resident 128-thread blocks per SM
+// requested from ptxas (__launch_bounds__), i.e. a register cap. Measured
+// defaults per representation dimension; 1 = no cap.
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 template <int D, bool REAL>
-void launch_hop(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream_t s) {
-  if (blocks <= 0) return;
+int default_minb() {
+  // profiles/r01_tune_minb_cfg*.log: a cap of 3 blocks/SM helps D = 2 and
+  // D = 3 (2-4 %); larger D spill under any cap.
+  return D <= 3 ? 3 : 1;
+}
+
+template <int D, bool REAL>
+int hop_blocks(int nsites, int npar) {
+  return (nsites + kBlock - 1) / kBlock * npar;
+}
+
+template <int D, bool REAL, int MINB>
+void launch_hop_minb(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream_t s) {
 #define LBCU_HOP_CASE(B, E)                                                         \
   if (bnd == B && epi == E) {                                                       \
-    hop_kernel<D, REAL, B, E><<<blocks, kBlock, 0, s>>>(A);                         \
+    hop_kernel<D, REAL, B, E, MINB><<<blocks, kBlock, 0, s>>>(A);                   \
     return;                                                                         \
   }
   LBCU_HOP_CASE(false, EPI_STORE)
@@ -295,6 +315,16 @@ void launch_hop(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream_t s)
   LBCU_HOP_CASE(true, EPI_STORE_NORM)
   LBCU_HOP_CASE(true, EPI_CG)
 #undef LBCU_HOP_CASE
+}
+
+template <int D, bool REAL>
+void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaStream_t s) {
+  if (nsites <= 0) return;
+  const int blocks = hop_blocks<D, REAL>(nsites, npar);
+  switch (env_int("LBCU_HOP_MINB", default_minb<D, REAL>())) {
+    case 3: launch_hop_minb<D, REAL, 3>(A, bnd, epi, blocks, s); return;
+    default: launch_hop_minb<D, REAL, 1>(A, bnd, epi, blocks, s); return;
+  }
 }
 
 template <int D, bool REAL>
@@ -376,17 +406,19 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   cudaStream_t s = ctx->stream;
 
   if (!geo.any_decomposed) {
-    const int bpp = static_cast<int>((geo.vh + kBlock - 1) / kBlock);
     A.nsites = static_cast<int>(geo.vh);
     A.both = npar == 2;
     A.par0 = pars[0];
-    const int blocks = bpp * npar;
+    int blocks = 0;
+    dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
+      blocks = hop_blocks<decltype(Dc)::value, decltype(Rc)::value>(A.nsites, npar);
+    });
     if (reduce) {
       if (blocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
       A.red = Reduce{ctx->partials, ctx->ticket, c.result, 0, blocks};
     }
     dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(A, false, c.epi, blocks, s);
+      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(A, false, c.epi, A.nsites, npar, s);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaGetLastError());
@@ -398,8 +430,10 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   int total_blocks = 0, bnd_off[2] = {0, 0}, int_blocks[2] = {0, 0}, bnd_blocks[2] = {0, 0};
   for (int k = 0; k < npar; ++k) {
     const int p = pars[k];
-    int_blocks[k] = (ctx->nint[p] + kBlock - 1) / kBlock;
-    bnd_blocks[k] = (ctx->nbnd[p] + kBlock - 1) / kBlock;
+    dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
+      int_blocks[k] = hop_blocks<decltype(Dc)::value, decltype(Rc)::value>(ctx->nint[p], 1);
+      bnd_blocks[k] = hop_blocks<decltype(Dc)::value, decltype(Rc)::value>(ctx->nbnd[p], 1);
+    });
     total_blocks += int_blocks[k] + bnd_blocks[k];
   }
   if (reduce && total_blocks > ctx->max_partials)
@@ -447,7 +481,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     if (reduce) Ai.red = Reduce{ctx->partials, ctx->ticket, c.result, off, total_blocks};
     LBCU_CUDA(cudaEventRecord(ctx->ev_pack, s));
     dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(Ai, false, c.epi, int_blocks[k], s);
+      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(Ai, false, c.epi, Ai.nsites, 1, s);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_pack, 0));
@@ -467,7 +501,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     bnd_off[k] = off + int_blocks[k];
     if (reduce) Ab.red = Reduce{ctx->partials, ctx->ticket, c.result, bnd_off[k], total_blocks};
     dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(Ab, true, c.epi, bnd_blocks[k], s);
+      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(Ab, true, c.epi, Ab.nsites, 1, s);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaGetLastError());
