@@ -74,14 +74,24 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def bytes_full_dphi(dr, real):  # 128 d + 32 c d^2 per site
-    c = 1 if real else 2
-    return 128 * dr + 32 * c * dr * dr
+def link_bytes(dr, real, fmt="full"):
+    """Bytes of one link as stored on the device (links.cuh)."""
+    return {"full": dr * dr * (8 if real else 16), "su2": 32, "r12": 96}[fmt]
 
 
-def bytes_eo_cg_iter(dr, real):  # per even site 4 B_hop + 11 * 64 d
-    c = 1 if real else 2
-    return 4 * (128 * dr + 64 * c * dr * dr) + 11 * 64 * dr
+def bytes_full_dphi(dr, real, fmt="full"):
+    """SURVEY.md §8(d) compulsory bytes per site of a full Dphi: spinor in + out
+    (128 d) + each of the 4 links of the site once; with fmt = "full" this is
+    SURVEY's 128 d + 32 c d^2."""
+    return 128 * dr + 4 * link_bytes(dr, real, fmt)
+
+
+def bytes_eo_hop(dr, real, fmt="full"):  # per output site: 128 d + 8 links
+    return 128 * dr + 8 * link_bytes(dr, real, fmt)
+
+
+def bytes_eo_cg_iter(dr, real, fmt="full"):  # SURVEY.md §8(d): per even site 4 B_hop + 11 * 64 d
+    return 4 * bytes_eo_hop(dr, real, fmt) + 11 * 64 * dr
 
 
 class ClockSampler:
@@ -216,8 +226,12 @@ def run_gpu(args, cfg):
     ctx = lb.Context(L, grid, rank, local if ws > 1 else 0, world)
     g = lb.init_gauge_random(L, n, rep, 1, grid=grid, rank=rank, links=links, eps=0.3)
     s = lb.init_spinor_random(L, dr, 1, 0, grid=grid, rank=rank)
-    gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g)
+    gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T)
+    if args.dense_links:
+        gauge.set_compact(False)
+    gauge.upload(g)
     del g
+    fmt, fmt_err = gauge.storage()
     a = lb.SpinorField(ctx, dr).upload(s)
     b = lb.SpinorField(ctx, dr)
 
@@ -253,10 +267,24 @@ def run_gpu(args, cfg):
     flops = fps * V * args.steps
     value = flops / (ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
-    bpsite = bytes_full_dphi(dr, real)
+    bpsite = bytes_full_dphi(dr, real, fmt)  # links counted as stored
     per_launch_bytes = bpsite * V / ws  # one Dphi kernel per rank per step (N = 1: a single launch)
     kernels_per_step = launches / args.steps
     achieved = bpsite * V / ws / (ms * 1e-3 / args.steps) / 1e9
+
+    # ---- the eo hop alone (the CG's dominant kernel) ------------------------
+    ae = lb.SpinorField(ctx, dr, lb.EVEN).upload(s)
+    bo = lb.SpinorField(ctx, dr, lb.ODD)
+    for _ in range(args.warmup):
+        lb.dphi_oe(bo, gauge, ae)
+    barrier()
+    ctx.event_record(4)
+    for _ in range(args.steps):
+        lb.dphi_oe(bo, gauge, ae)
+    ctx.event_record(5)
+    barrier()
+    hop_ms = max_over_ranks(ctx.elapsed_ms(4, 5)) / args.steps
+    hop_gbs = bytes_eo_hop(dr, real, fmt) * V / 2 / ws / (hop_ms * 1e-3) / 1e9
 
     # ---- end to end through the C-ABI with host buffers ---------------------
     import torch
@@ -290,7 +318,7 @@ def run_gpu(args, cfg):
         barrier()
         o = lb.cg_solve_eo(gauge, mass, rhs, st)
         secs = max_over_ranks(o.seconds)
-        cg_bytes = (o.iterations * bytes_eo_cg_iter(dr, real) + 2 * (128 * dr + 64 * (1 if real else 2) * dr * dr)
+        cg_bytes = (o.iterations * bytes_eo_cg_iter(dr, real, fmt) + 2 * bytes_eo_hop(dr, real, fmt)
                     + 3 * 64 * dr) * V / 2
         cg = {"solver": "eo CG on Mhat^dag Mhat", "tolerance": cfg["tol"], "iterations": o.iterations,
               "seconds": secs, "true_rel_residual": o.true_rel_residual,
@@ -326,9 +354,14 @@ def run_gpu(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": per_launch_bytes,
+                         "bytes_per_site": bpsite,
+                         "link_storage": fmt, "link_reconstruction_err": fmt_err,
+                         "survey_model_bytes_per_site": bytes_full_dphi(dr, real, "full"),
                          "kernel": "hop_kernel (full Dphi, both parities)",
                          "kernels_per_step": kernels_per_step,
-                         "traffic": traffic_from_profiles(f"cfg{args.config}_dphi")},
+                         "traffic": traffic_from_profiles(f"cfg{args.config}_dphi_{fmt}"),
+                         "eo_hop": {"ms": hop_ms, "achieved": hop_gbs, "frac": hop_gbs / peak,
+                                    "bytes_per_output_site": bytes_eo_hop(dr, real, fmt)}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes, "steps": e2e_steps},
@@ -352,6 +385,7 @@ def main():
     ap.add_argument("--no-cg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dense-links", action="store_true", help="store links as dense matrices")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]

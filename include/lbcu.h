@@ -135,6 +135,15 @@ int lbcu_gauge_create(lbcu_ctx c, int group_rank, int rep, int bc_time, lbcu_gau
  * antiperiodic sign to U_0 on the last global time slice on the device. */
 int lbcu_gauge_upload(lbcu_gauge g, const double* host);
 int lbcu_gauge_download(lbcu_gauge g, double* host); /* as uploaded (no BC sign) */
+/* Link storage on the device. Compact exact forms are used when every
+ * uploaded link reconstructs to within 1e-12 (checked at upload):
+ *   LBCU_GAUGE_SU2 : SU(2) links as 2 complex (fundamental; adjoint rebuilt)
+ *   LBCU_GAUGE_R12 : SU(3) fundamental, two rows (third = conj(r0 x r1))
+ * otherwise LBCU_GAUGE_FULL (dense dr x dr). set_compact(0) before upload
+ * forces dense storage. */
+enum lbcu_gauge_format { LBCU_GAUGE_FULL = 0, LBCU_GAUGE_SU2 = 1, LBCU_GAUGE_R12 = 2 };
+int lbcu_gauge_set_compact(lbcu_gauge g, int enable);
+int lbcu_gauge_storage(lbcu_gauge g, int* format, double* reconstruction_error);
 int lbcu_gauge_destroy(lbcu_gauge g);
 
 /* ---- spinor fields: SpinorField ------------------------------------------ */

@@ -143,6 +143,8 @@ def lib():
             "lbcu_gauge_upload": (C.c_int, [_vp, _dp]),
             "lbcu_gauge_download": (C.c_int, [_vp, _dp]),
             "lbcu_gauge_destroy": (C.c_int, [_vp]),
+            "lbcu_gauge_set_compact": (C.c_int, [_vp, C.c_int]),
+            "lbcu_gauge_storage": (C.c_int, [_vp, _ip, _dp]),
             "lbcu_spinor_create": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
             "lbcu_spinor_upload": (C.c_int, [_vp, _dp]),
             "lbcu_spinor_download": (C.c_int, [_vp, _dp]),
@@ -373,6 +375,17 @@ class GaugeField:
             raise ContractViolation(f"gauge upload expects {self.host_shape}, got {a.shape}")
         _check(lib().lbcu_gauge_upload(self._h, a.ctypes.data_as(_dp)))
         return self
+
+    def set_compact(self, enable: bool):
+        """Allow (default) or forbid compact link storage for later uploads."""
+        _check(lib().lbcu_gauge_set_compact(self._h, int(bool(enable))))
+        return self
+
+    def storage(self):
+        """(format name, max reconstruction error at the last upload)."""
+        f, e = C.c_int(), C.c_double()
+        _check(lib().lbcu_gauge_storage(self._h, C.byref(f), C.byref(e)))
+        return {0: "full", 1: "su2", 2: "r12"}[f.value], e.value
 
     def download(self) -> np.ndarray:
         dt = np.float64 if self.real_links else np.complex128

@@ -393,9 +393,10 @@ int lbcu_gauge_create(lbcu_ctx c, int group_rank, int rep, int bc_time, lbcu_gau
     throw Error(LBCU_CONFIG_ERROR, "unknown time boundary condition");
   g->bc = bc_time;
   const size_t esz = g->real ? sizeof(double) : sizeof(double2);
-  g->bytes = 2 * 4 * static_cast<size_t>(g->dr) * g->dr * c->geo.stride * esz;
-  LBCU_CUDA(cudaMalloc(&g->base, g->bytes));
-  LBCU_CUDA(cudaMemsetAsync(g->base, 0, g->bytes, c->stream));
+  const size_t bytes = 2 * 4 * static_cast<size_t>(g->dr) * g->dr * c->geo.stride * esz;
+  LBCU_CUDA(cudaMalloc(&g->base, bytes));  // make_gauge: zero links until uploaded
+  LBCU_CUDA(cudaMemsetAsync(g->base, 0, bytes, c->stream));
+  g->fmt = 0;
   *out = g.release();
   API_END
 }
@@ -413,6 +414,21 @@ int lbcu_gauge_download(lbcu_gauge g, double* host) {
   need(g && host, "lbcu_gauge_download: null argument");
   bind(g->ctx);
   gauge_download(g->ctx, g, host);
+  API_END
+}
+
+int lbcu_gauge_set_compact(lbcu_gauge g, int enable) {
+  API_BEGIN
+  need(g != nullptr, "lbcu_gauge_set_compact: null gauge");
+  g->compact_ok = enable != 0;
+  API_END
+}
+
+int lbcu_gauge_storage(lbcu_gauge g, int* format, double* reconstruction_error) {
+  API_BEGIN
+  need(g != nullptr, "lbcu_gauge_storage: null gauge");
+  if (format) *format = g->fmt;
+  if (reconstruction_error) *reconstruction_error = g->compact_err;
   API_END
 }
 

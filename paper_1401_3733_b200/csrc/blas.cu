@@ -7,6 +7,10 @@
 // double2 array (padding kept at zero), so every vector op is a flat,
 // coalesced grid-stride loop with 128-bit accesses; reductions are
 // deterministic (fixed-order block partials, see device.cuh).
+#include <cstdlib>
+#include <cstring>
+
+#include "links.cuh"
 #include "objects.hpp"
 
 namespace lbcu {
@@ -362,42 +366,248 @@ void spinor_download(lbcu_ctx_s* ctx, const lbcu_spinor_s* s, double* host) {
   LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
-void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host) {
-  const int nv = 4 * g->dr * g->dr;
-  const size_t esz = g->real ? sizeof(double) : sizeof(double2);
-  const size_t bytes = static_cast<size_t>(ctx->geo.volume) * nv * esz;
-  ensure_staging(ctx, bytes);
-  LBCU_CUDA(cudaMemcpyAsync(ctx->staging, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  const int sign = g->bc == LBCU_BC_ANTIPERIODIC_T ? g->dr * g->dr : 0;
-  const size_t pstride = static_cast<size_t>(nv) * ctx->geo.stride;
-  if (g->real) {
-    double* b = static_cast<double*>(g->base);
-    launch_to_soa<double>(ctx, static_cast<const double*>(ctx->staging), b, b + pstride, nv, sign);
-  } else {
-    double2* b = static_cast<double2*>(g->base);
-    launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b, b + pstride, nv, sign);
+// ---- gauge storage: upload, compression to the compact formats, download --
+namespace {
+
+// compact format available for a representation (links.cuh)
+int compact_format(const lbcu_gauge_s* g) {
+  if (g->dr == 2 && !g->real) return GF_SU2;  // SU(2) fundamental
+  if (g->dr == 3 && g->real && g->n == 2) return GF_SU2;  // SU(2) adjoint
+  if (g->dr == 3 && !g->real && g->n == 3 && g->rep == LBCU_REP_FUNDAMENTAL) return GF_R12;
+  return GF_FULL;
+}
+
+int fmt_entries(int fmt, int dr) { return fmt == GF_SU2 ? 2 : fmt == GF_R12 ? 6 : dr * dr; }
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double v) {
+  atomicMax(p, __double_as_longlong(v));  // non-negative doubles order like their bit patterns
+}
+
+__device__ __forceinline__ double cabs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+
+// full dense link -> compact storage, with the reconstruction error
+template <int D, bool REAL, int FMT>
+__global__ void k_compress(const LinkT<REAL>* __restrict__ full, double2* __restrict__ compact,
+                           long long stride, int vh, unsigned long long* err) {
+  constexpr int E = LinkFmt<D, REAL, FMT>::entries;
+  const long long n = 8LL * vh;  // (parity, mu) blocks x sites
+  double worst = 0.0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const long long blk = t / vh, cb = t % vh;
+    const LinkT<REAL>* f = full + blk * D * D * stride + cb;
+    double2* cp = compact + blk * E * stride + cb;
+    LinkT<REAL> u[D * D];
+#pragma unroll
+    for (int e = 0; e < D * D; ++e) u[e] = f[(long long)e * stride];
+    double2 st[E];
+    if constexpr (FMT == GF_SU2 && !REAL) {
+      st[0] = u[0];
+      st[1] = u[1];
+    } else if constexpr (FMT == GF_SU2 && REAL) {
+      // SO(3) -> unit quaternion (w, v) with R = (w^2-|v|^2) I + 2 v v^T + 2 w [v]x,
+      // Shepperd's branch choice; then a0 = w, a = -v (links.cuh convention)
+      const double tr = u[0] + u[4] + u[8];
+      double w, vx, vy, vz;
+      if (tr > 0) {
+        w = 0.5 * sqrt(1.0 + tr);
+        vx = (u[7] - u[5]) / (4 * w);
+        vy = (u[2] - u[6]) / (4 * w);
+        vz = (u[3] - u[1]) / (4 * w);
+      } else if (u[0] >= u[4] && u[0] >= u[8]) {
+        vx = 0.5 * sqrt(fmax(0.0, 1.0 + u[0] - u[4] - u[8]));
+        w = (u[7] - u[5]) / (4 * vx);
+        vy = (u[1] + u[3]) / (4 * vx);
+        vz = (u[2] + u[6]) / (4 * vx);
+      } else if (u[4] >= u[8]) {
+        vy = 0.5 * sqrt(fmax(0.0, 1.0 + u[4] - u[0] - u[8]));
+        w = (u[2] - u[6]) / (4 * vy);
+        vx = (u[1] + u[3]) / (4 * vy);
+        vz = (u[5] + u[7]) / (4 * vy);
+      } else {
+        vz = 0.5 * sqrt(fmax(0.0, 1.0 + u[8] - u[0] - u[4]));
+        w = (u[3] - u[1]) / (4 * vz);
+        vx = (u[2] + u[6]) / (4 * vz);
+        vy = (u[5] + u[7]) / (4 * vz);
+      }
+      st[0] = make_double2(w, -vz);   // al = a0 + i a3
+      st[1] = make_double2(-vy, -vx); // be = a2 + i a1
+    } else {
+#pragma unroll
+      for (int e = 0; e < 6; ++e) st[e] = u[e];
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) cp[(long long)e * stride] = st[e];
+    // validate: rebuild from the stored entries and compare with the dense link
+    LinkT<REAL> r[D * D];
+    build_link<D, REAL, FMT>(r, st);
+#pragma unroll
+    for (int e = 0; e < D * D; ++e) {
+      double d;
+      if constexpr (REAL) d = fabs(r[e] - u[e]);
+      else d = sqrt(cabs2(make_double2(r[e].x - u[e].x, r[e].y - u[e].y)));
+      worst = fmax(worst, d);
+    }
   }
+  if (worst > 0.0 || !isfinite(worst)) atomic_max_nonneg(err, isfinite(worst) ? worst : 1e300);
+}
+
+// compact -> dense (downloads)
+template <int D, bool REAL, int FMT>
+__global__ void k_expand(const double2* __restrict__ compact, LinkT<REAL>* __restrict__ full,
+                         long long stride, int vh) {
+  constexpr int E = LinkFmt<D, REAL, FMT>::entries;
+  const long long n = 8LL * vh;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const long long blk = t / vh, cb = t % vh;
+    LinkT<REAL> u[D * D];
+    load_link<D, REAL, FMT>(u, compact + blk * E * stride + cb, stride);
+#pragma unroll
+    for (int e = 0; e < D * D; ++e) full[blk * D * D * stride + (long long)e * stride + cb] = u[e];
+  }
+}
+
+// antiperiodic time: negate U_0 on the last global time slice (dense storage)
+template <class T>
+__global__ void k_bake_sign(T* full, long long stride, int entries, DevGeo g, int t_off, int tlast) {
+  const long long n = 2LL * g.vh;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const int par = static_cast<int>(t / g.vh), cb = static_cast<int>(t % g.vh);
+    int c[4], s;
+    cb_coords(g, cb, par, c, s);
+    if (c[0] + t_off != tlast) continue;
+    T* base = full + (long long)par * 4 * entries * stride + cb;  // mu = 0 block
+    for (int e = 0; e < entries; ++e) base[(long long)e * stride] = neg(base[(long long)e * stride]);
+  }
+}
+
+template <class F>
+void dispatch_compact(const lbcu_gauge_s* g, int fmt, F&& f) {
+  using std::integral_constant;
+  if (fmt == GF_SU2 && !g->real)
+    return f(integral_constant<int, 2>{}, std::false_type{}, integral_constant<int, GF_SU2>{});
+  if (fmt == GF_SU2 && g->real)
+    return f(integral_constant<int, 3>{}, std::true_type{}, integral_constant<int, GF_SU2>{});
+  if (fmt == GF_R12)
+    return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_R12>{});
+  throw Error(LBCU_CONTRACT_VIOLATION, "no compact gauge format");
+}
+
+int grid_for(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148 * 16)); }
+
+bool compaction_enabled(const lbcu_gauge_s* g) {
+  const char* e = std::getenv("LBCU_GAUGE_COMPACT");
+  return g->compact_ok && !(e && e[0] == '0');
+}
+
+}  // namespace
+
+void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host) {
+  const Geometry& geo = ctx->geo;
+  const int dd = g->dr * g->dr;
+  const int nv = 4 * dd;
+  const size_t esz = g->real ? sizeof(double) : sizeof(double2);
+  const size_t bytes = static_cast<size_t>(geo.volume) * nv * esz;
+  const size_t full_bytes = 2 * static_cast<size_t>(nv) * geo.stride * esz;
+  ensure_staging(ctx, bytes);
+  void* full = nullptr;
+  if (g->fmt == GF_FULL && g->base) {
+    full = g->base;
+  } else {
+    LBCU_CUDA(cudaMalloc(&full, full_bytes));
+    LBCU_CUDA(cudaMemsetAsync(full, 0, full_bytes, ctx->stream));
+  }
+  LBCU_CUDA(cudaMemcpyAsync(ctx->staging, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const size_t pstride = static_cast<size_t>(nv) * geo.stride;
+  if (g->real) {
+    double* b = static_cast<double*>(full);
+    launch_to_soa<double>(ctx, static_cast<const double*>(ctx->staging), b, b + pstride, nv, 0);
+  } else {
+    double2* b = static_cast<double2*>(full);
+    launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b, b + pstride, nv, 0);
+  }
+  auto adopt = [&](void* base, int fmt) {
+    if (g->base && g->base != base) LBCU_CUDA(cudaFree(g->base));
+    g->base = base;
+    g->fmt = fmt;
+  };
+  const int cf = compact_format(g);
+  if (cf != GF_FULL && compaction_enabled(g)) {
+    const size_t cbytes = 2 * 4 * static_cast<size_t>(fmt_entries(cf, g->dr)) * geo.stride * sizeof(double2);
+    void* compact = nullptr;
+    LBCU_CUDA(cudaMalloc(&compact, cbytes));
+    LBCU_CUDA(cudaMemsetAsync(compact, 0, cbytes, ctx->stream));
+    unsigned long long* derr = reinterpret_cast<unsigned long long*>(ctx->dscal + 60);
+    LBCU_CUDA(cudaMemsetAsync(derr, 0, sizeof(unsigned long long), ctx->stream));
+    dispatch_compact(g, cf, [&](auto Dc, auto Rc, auto Fc) {
+      constexpr int D = decltype(Dc)::value;
+      constexpr bool REAL = decltype(Rc)::value;
+      k_compress<D, REAL, decltype(Fc)::value><<<grid_for(8LL * geo.vh), 256, 0, ctx->stream>>>(
+          static_cast<const LinkT<REAL>*>(full), static_cast<double2*>(compact), geo.stride,
+          static_cast<int>(geo.vh), derr);
+    });
+    ctx->launches++;
+    LBCU_CUDA(cudaGetLastError());
+    unsigned long long bits = 0;
+    LBCU_CUDA(cudaMemcpyAsync(&bits, derr, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream));
+    LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+    double err;
+    std::memcpy(&err, &bits, sizeof(err));
+    g->compact_err = err;
+    if (err <= 1e-12) {
+      if (full != g->base) LBCU_CUDA(cudaFree(full));
+      adopt(compact, cf);  // frees the previous storage
+      return;
+    }
+    LBCU_CUDA(cudaFree(compact));
+  }
+  if (g->bc == LBCU_BC_ANTIPERIODIC_T) {
+    const int t_off = geo.coords[0] * geo.local[0];
+    if (g->real)
+      k_bake_sign<double><<<grid_for(2 * geo.vh), 256, 0, ctx->stream>>>(
+          static_cast<double*>(full), geo.stride, dd, ctx->dgeo, t_off, geo.global[0] - 1);
+    else
+      k_bake_sign<double2><<<grid_for(2 * geo.vh), 256, 0, ctx->stream>>>(
+          static_cast<double2*>(full), geo.stride, dd, ctx->dgeo, t_off, geo.global[0] - 1);
+    ctx->launches++;
+    LBCU_CUDA(cudaGetLastError());
+  }
+  adopt(full, GF_FULL);
   // the staging buffer is reused by the next transfer: finish this one first
   LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host) {
+  const Geometry& geo = ctx->geo;
   const int nv = 4 * g->dr * g->dr;
   const size_t esz = g->real ? sizeof(double) : sizeof(double2);
-  const size_t bytes = static_cast<size_t>(ctx->geo.volume) * nv * esz;
+  const size_t bytes = static_cast<size_t>(geo.volume) * nv * esz;
   ensure_staging(ctx, bytes);
-  const size_t pstride = static_cast<size_t>(nv) * ctx->geo.stride;
+  const size_t pstride = static_cast<size_t>(nv) * geo.stride;
+  const void* full = g->base;
+  void* tmp = nullptr;
+  if (g->fmt != GF_FULL) {
+    LBCU_CUDA(cudaMalloc(&tmp, 2 * pstride * esz));
+    dispatch_compact(g, g->fmt, [&](auto Dc, auto Rc, auto Fc) {
+      constexpr int D = decltype(Dc)::value;
+      constexpr bool REAL = decltype(Rc)::value;
+      k_expand<D, REAL, decltype(Fc)::value><<<grid_for(8LL * geo.vh), 256, 0, ctx->stream>>>(
+          static_cast<const double2*>(g->base), static_cast<LinkT<REAL>*>(tmp), geo.stride,
+          static_cast<int>(geo.vh));
+    });
+    ctx->launches++;
+    full = tmp;
+  }
   if (g->real) {
-    const double* b = static_cast<const double*>(g->base);
+    const double* b = static_cast<const double*>(full);
     launch_to_aos<double>(ctx, b, b + pstride, static_cast<double*>(ctx->staging), nv);
   } else {
-    const double2* b = static_cast<const double2*>(g->base);
+    const double2* b = static_cast<const double2*>(full);
     launch_to_aos<double2>(ctx, b, b + pstride, static_cast<double2*>(ctx->staging), nv);
   }
   LBCU_CUDA(cudaMemcpyAsync(host, ctx->staging, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (g->bc == LBCU_BC_ANTIPERIODIC_T) {  // report the links as uploaded (undo the BC sign)
-    const Geometry& geo = ctx->geo;
+  if (tmp) LBCU_CUDA(cudaFree(tmp));
+  if (g->fmt == GF_FULL && g->bc == LBCU_BC_ANTIPERIODIC_T) {  // report the links as uploaded
     const int per = nv * (g->real ? 1 : 2);
     const int64_t slab = geo.volume / geo.local[0];
     if (geo.coords[0] == geo.grid[0] - 1)

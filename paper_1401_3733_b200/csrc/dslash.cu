@@ -15,7 +15,8 @@
 //
 // Memory layout: every spinor component / link entry is a contiguous
 // double2 (or double for real links) array over checkerboard sites, so a warp
-// issues fully coalesced 512-byte (LDG.128) loads for each component.
+// issues fully coalesced 512-byte (LDG.128) loads for each component. Links
+// are read in their storage format (links.cuh) and rebuilt in registers.
 //
 // Decomposed directions: boundary sites are handled by a second launch that
 // reads half-spinor halos produced by pack_kernel on the neighbour rank:
@@ -25,6 +26,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "links.cuh"
 #include "objects.hpp"
 
 namespace lbcu {
@@ -37,7 +39,7 @@ struct HopArgs {
   double2* out[2];       // output blocks by output parity
   const double2* x[2];   // diagonal-term blocks by output parity (nullable)
   double2* r[2];         // CG residual blocks by output parity
-  const void* gauge;     // [2][4][D*D][stride]
+  const void* gauge;     // [2 parity][4 mu][entries][stride] in the storage format
   double a, b, s5in, s5x, s5acc;
   const double* alpha;
   int par0;    // output parity of a single-parity launch
@@ -47,41 +49,11 @@ struct HopArgs {
   const double2* hfwd[4];
   const double2* hbwd[4];
   int hcount[4];
+  // antiperiodic time sign applied in-kernel (compact formats): the U_0 link
+  // whose global time coordinate is bc_tlast carries a factor -1
+  int bc_kernel, t_off, bc_tlast;
   Reduce red;
 };
-
-template <bool REAL>
-using LinkT = std::conditional_t<REAL, double, double2>;
-
-template <int D, bool REAL>
-__device__ __forceinline__ void umul(double2 (&g)[2][D], const LinkT<REAL>* __restrict__ U,
-                                     long long st, int site, const double2 (&h)[2][D],
-                                     bool dagger) {
-#pragma unroll
-  for (int r = 0; r < D; ++r) {
-    g[0][r] = make_double2(0.0, 0.0);
-    g[1][r] = make_double2(0.0, 0.0);
-  }
-#pragma unroll
-  for (int r = 0; r < D; ++r)
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      if constexpr (REAL) {
-        const double u = ldg(U + (long long)(dagger ? c * D + r : r * D + c) * st + site);
-        rmac(g[0][r], u, h[0][c]);
-        rmac(g[1][r], u, h[1][c]);
-      } else {
-        const double2 u = ldg(U + (long long)(dagger ? c * D + r : r * D + c) * st + site);
-        if (dagger) {
-          cmac_conj(g[0][r], u, h[0][c]);
-          cmac_conj(g[1][r], u, h[1][c]);
-        } else {
-          cmac(g[0][r], u, h[0][c]);
-          cmac(g[1][r], u, h[1][c]);
-        }
-      }
-    }
-}
 
 template <int D, int R0, int R1, int Q0, int Q1>
 __device__ __forceinline__ void reconstruct(double2 (&acc)[4][D], const double2 (&g)[2][D]) {
@@ -109,16 +81,31 @@ __device__ __forceinline__ void project(double2 (&h)[2][D], const double2* __res
   }
 }
 
-template <int D, bool REAL, bool BND, int MU>
+template <int D>
+__device__ __forceinline__ void negate(double2 (&h)[2][D]) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) h[a][c] = make_double2(-h[a][c].x, -h[a][c].y);
+}
+
+template <int D, bool REAL, int FMT>
+using ElemT = typename LinkFmt<D, REAL, FMT>::Elem;
+
+// pointer to entry 0 of the (parity, mu) link block at cb site `site`
+template <int D, bool REAL, int FMT>
+__device__ __forceinline__ const ElemT<D, REAL, FMT>* link_ptr(const void* gauge, long long st,
+                                                               int par, int mu, int site) {
+  constexpr int E = LinkFmt<D, REAL, FMT>::entries;
+  return static_cast<const ElemT<D, REAL, FMT>*>(gauge) + (long long)(par * 4 + mu) * E * st + site;
+}
+
+template <int D, bool REAL, int FMT, bool BND, int MU>
 __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
-                                       const double2* __restrict__ in,
-                                       const LinkT<REAL>* __restrict__ Uown,
-                                       const LinkT<REAL>* __restrict__ Uoth, int i, int s,
+                                       const double2* __restrict__ in, int par, int i, int s,
                                        const int c[4]) {
   using G = Gam<MU>;
   const long long st = A.g.stride;
-  const LinkT<REAL>* Uo = Uown + (long long)MU * D * D * st;
-  const LinkT<REAL>* Ub = Uoth + (long long)MU * D * D * st;
   {  // forward: (1 - g_mu) U_mu(x) in(x + mu)
     double2 h[2][D], g[2][D];
     if (BND && !A.g.wrap[MU] && c[MU] == A.g.L[MU] - 1) {
@@ -131,7 +118,8 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
     } else {
       project<D, G::p0, G::p1, G::f0, G::f1>(h, in, st, nb_fwd(A.g, s, c, MU) >> 1, A.s5in);
     }
-    umul<D, REAL>(g, Uo, st, i, h, false);
+    if (MU == 0 && A.bc_kernel && A.t_off + c[0] == A.bc_tlast) negate<D>(h);
+    link_mul<D, REAL, FMT, false>(g, link_ptr<D, REAL, FMT>(A.gauge, st, par, MU, i), st, h);
     reconstruct<D, G::r0, G::r1, G::q0, G::q1>(acc, g);
   }
   {  // backward: (1 + g_mu) U_mu(x - mu)^dag in(x - mu)
@@ -147,13 +135,17 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
       double2 h[2][D];
       const int nb = nb_bwd(A.g, s, c, MU) >> 1;
       project<D, G::p0, G::p1, G::f0 ^ 1, G::f1 ^ 1>(h, in, st, nb, A.s5in);
-      umul<D, REAL>(g, Ub, st, nb, h, true);
+      if (MU == 0 && A.bc_kernel) {
+        const int tl = c[0] > 0 ? c[0] - 1 : A.g.L[0] - 1;
+        if (A.t_off + tl == A.bc_tlast) negate<D>(h);
+      }
+      link_mul<D, REAL, FMT, true>(g, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, MU, nb), st, h);
     }
     reconstruct<D, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, g);
   }
 }
 
-template <int D, bool REAL, bool BND, int EPI, int MINB>
+template <int D, bool REAL, int FMT, bool BND, int EPI, int MINB>
 __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ HopArgs A) {
   int par, idx;
   if (A.both) {
@@ -174,14 +166,11 @@ __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ 
 #pragma unroll
       for (int cc = 0; cc < D; ++cc) acc[k][cc] = make_double2(0.0, 0.0);
     const long long st = A.g.stride;
-    const LinkT<REAL>* Ug = static_cast<const LinkT<REAL>*>(A.gauge);
-    const LinkT<REAL>* Uown = Ug + (long long)par * 4 * D * D * st;
-    const LinkT<REAL>* Uoth = Ug + (long long)(par ^ 1) * 4 * D * D * st;
     const double2* in = A.in[par ^ 1];
-    hop_mu<D, REAL, BND, 0>(acc, A, in, Uown, Uoth, i, s, c);
-    hop_mu<D, REAL, BND, 1>(acc, A, in, Uown, Uoth, i, s, c);
-    hop_mu<D, REAL, BND, 2>(acc, A, in, Uown, Uoth, i, s, c);
-    hop_mu<D, REAL, BND, 3>(acc, A, in, Uown, Uoth, i, s, c);
+    hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
+    hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
+    hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
+    hop_mu<D, REAL, FMT, BND, 3>(acc, A, in, par, i, s, c);
 
     const double2* x = A.x[par];
     double2* out = A.out[par];
@@ -222,10 +211,11 @@ struct PackArgs {
   const void* gauge;
   int in_par, mu, dir, count;
   double s5in;
+  int bc_kernel, t_off, bc_tlast;
   double2* outbuf;  // [2D][count]
 };
 
-template <int D, bool REAL, int MU>
+template <int D, bool REAL, int FMT, int MU>
 __device__ __forceinline__ void pack_site(const PackArgs& P, int j) {
   using G = Gam<MU>;
   const long long st = P.g.stride;
@@ -256,10 +246,9 @@ __device__ __forceinline__ void pack_site(const PackArgs& P, int j) {
       for (int cc = 0; cc < D; ++cc) P.outbuf[(a * D + cc) * P.count + j] = h[a][cc];
   } else {
     project<D, G::p0, G::p1, G::f0 ^ 1, G::f1 ^ 1>(h, P.in, st, cb, P.s5in);
+    if (MU == 0 && P.bc_kernel && P.t_off + c[0] == P.bc_tlast) negate<D>(h);
     double2 g[2][D];
-    const LinkT<REAL>* U =
-        static_cast<const LinkT<REAL>*>(P.gauge) + (long long)(P.in_par * 4 + MU) * D * D * st;
-    umul<D, REAL>(g, U, st, cb, h, true);
+    link_mul<D, REAL, FMT, true>(g, link_ptr<D, REAL, FMT>(P.gauge, st, P.in_par, MU, cb), st, h);
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -267,45 +256,44 @@ __device__ __forceinline__ void pack_site(const PackArgs& P, int j) {
   }
 }
 
-template <int D, bool REAL>
+template <int D, bool REAL, int FMT>
 __global__ void __launch_bounds__(128) pack_kernel(const __grid_constant__ PackArgs P) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.count) return;
   switch (P.mu) {
-    case 0: pack_site<D, REAL, 0>(P, j); break;
-    case 1: pack_site<D, REAL, 1>(P, j); break;
-    case 2: pack_site<D, REAL, 2>(P, j); break;
-    default: pack_site<D, REAL, 3>(P, j); break;
+    case 0: pack_site<D, REAL, FMT, 0>(P, j); break;
+    case 1: pack_site<D, REAL, FMT, 1>(P, j); break;
+    case 2: pack_site<D, REAL, FMT, 2>(P, j); break;
+    default: pack_site<D, REAL, FMT, 3>(P, j); break;
   }
 }
 
 constexpr int kBlock = 128;
 
 // Occupancy knob: LBCU_HOP_MINB = minimum resident 128-thread blocks per SM
-// requested from ptxas (__launch_bounds__), i.e. a register cap. Measured
-// defaults per representation dimension; 1 = no cap.
+// requested from ptxas (__launch_bounds__), i.e. a register cap.
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
 }
 
-template <int D, bool REAL>
+template <int D, bool REAL, int FMT>
 int default_minb() {
-  // profiles/r01_tune_minb_cfg*.log: a cap of 3 blocks/SM helps D = 2 and
-  // D = 3 (2-4 %); larger D spill under any cap.
-  return D <= 3 ? 3 : 1;
+  // profiles/r01_tune_*: a cap of 3 blocks/SM helps D = 2 (13 % with SU(2)
+  // links) and the real adjoint; dense/R12 SU(3) runs best uncapped on the eo
+  // hop; larger D spill under any cap.
+  if (D == 2 || (D == 3 && REAL)) return 3;
+  if (D == 3 && FMT == GF_FULL) return 3;
+  return 1;
 }
 
-template <int D, bool REAL>
-int hop_blocks(int nsites, int npar) {
-  return (nsites + kBlock - 1) / kBlock * npar;
-}
+int hop_blocks(int nsites, int npar) { return (nsites + kBlock - 1) / kBlock * npar; }
 
-template <int D, bool REAL, int MINB>
+template <int D, bool REAL, int FMT, int MINB>
 void launch_hop_minb(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream_t s) {
 #define LBCU_HOP_CASE(B, E)                                                         \
   if (bnd == B && epi == E) {                                                       \
-    hop_kernel<D, REAL, B, E, MINB><<<blocks, kBlock, 0, s>>>(A);                   \
+    hop_kernel<D, REAL, FMT, B, E, MINB><<<blocks, kBlock, 0, s>>>(A);              \
     return;                                                                         \
   }
   LBCU_HOP_CASE(false, EPI_STORE)
@@ -317,43 +305,50 @@ void launch_hop_minb(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream
 #undef LBCU_HOP_CASE
 }
 
-template <int D, bool REAL>
+template <int D, bool REAL, int FMT>
 void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaStream_t s) {
   if (nsites <= 0) return;
-  const int blocks = hop_blocks<D, REAL>(nsites, npar);
-  switch (env_int("LBCU_HOP_MINB", default_minb<D, REAL>())) {
-    case 3: launch_hop_minb<D, REAL, 3>(A, bnd, epi, blocks, s); return;
-    default: launch_hop_minb<D, REAL, 1>(A, bnd, epi, blocks, s); return;
+  const int blocks = hop_blocks(nsites, npar);
+  if constexpr (D <= 3) {
+    if (env_int("LBCU_HOP_MINB", default_minb<D, REAL, FMT>()) == 3) {
+      launch_hop_minb<D, REAL, FMT, 3>(A, bnd, epi, blocks, s);
+      return;
+    }
   }
+  launch_hop_minb<D, REAL, FMT, 1>(A, bnd, epi, blocks, s);
 }
 
-template <int D, bool REAL>
-void launch_pack(const PackArgs& P, cudaStream_t s) {
-  pack_kernel<D, REAL><<<(P.count + kBlock - 1) / kBlock, kBlock, 0, s>>>(P);
-}
-
-// Supported representation dimensions (compile-time specialisations).
-// complex: SU(2)F 2, SU(3)F/SU(3)AS 3, SU(4)F 4, SU(4)AS/SU(3)S/SU(6)F 6,
-//          SU(4)S 10; real: SU(2)A 3, SU(3)A 8.
+// Supported representation dimensions and storage formats (compile-time
+// specialisations). complex: SU(2)F 2, SU(3)F/SU(3)AS 3, SU(4)F 4,
+// SU(4)AS/SU(3)S/SU(6)F 6, SU(4)S 10; real: SU(2)A 3, SU(3)A 8.
 template <class F>
-void dispatch_rep(int dr, bool real, F&& f) {
+void dispatch(int dr, bool real, int fmt, F&& f) {
+  using std::integral_constant;
   if (!real) {
     switch (dr) {
-      case 2: f(std::integral_constant<int, 2>{}, std::false_type{}); return;
-      case 3: f(std::integral_constant<int, 3>{}, std::false_type{}); return;
-      case 4: f(std::integral_constant<int, 4>{}, std::false_type{}); return;
-      case 6: f(std::integral_constant<int, 6>{}, std::false_type{}); return;
-      case 10: f(std::integral_constant<int, 10>{}, std::false_type{}); return;
+      case 2:
+        if (fmt == GF_SU2) return f(integral_constant<int, 2>{}, std::false_type{}, integral_constant<int, GF_SU2>{});
+        return f(integral_constant<int, 2>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
+      case 3:
+        if (fmt == GF_R12) return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_R12>{});
+        return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
+      case 4: return f(integral_constant<int, 4>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
+      case 6: return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
+      case 10: return f(integral_constant<int, 10>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
     }
   } else {
     switch (dr) {
-      case 3: f(std::integral_constant<int, 3>{}, std::true_type{}); return;
-      case 8: f(std::integral_constant<int, 8>{}, std::true_type{}); return;
+      case 3:
+        if (fmt == GF_SU2) return f(integral_constant<int, 3>{}, std::true_type{}, integral_constant<int, GF_SU2>{});
+        return f(integral_constant<int, 3>{}, std::true_type{}, integral_constant<int, GF_FULL>{});
+      case 8: return f(integral_constant<int, 8>{}, std::true_type{}, integral_constant<int, GF_FULL>{});
     }
   }
   throw Error(LBCU_CONFIG_ERROR, "no device specialisation for representation dimension " +
                                      std::to_string(dr) + (real ? " (real)" : " (complex)"));
 }
+
+#define LBCU_TPARAMS(Dc, Rc, Fc) decltype(Dc)::value, decltype(Rc)::value, decltype(Fc)::value
 
 HaloBufs& halo_bufs(lbcu_ctx_s* ctx, int dr) {
   HaloBufs& hb = ctx->halo[dr];
@@ -379,6 +374,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   const Geometry& geo = ctx->geo;
   const int dr = c.in->dr;
   const bool real = c.g->real;
+  const int fmt = c.g->fmt;
   const int pars[2] = {c.out_parity == 2 ? 0 : c.out_parity, c.out_parity == 2 ? 1 : c.out_parity};
   const int npar = c.out_parity == 2 ? 2 : 1;
   for (int k = 0; k < npar; ++k) {
@@ -402,6 +398,9 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   A.s5x = c.s5x;
   A.s5acc = c.s5acc;
   A.alpha = c.alpha;
+  A.bc_kernel = (c.g->bc == LBCU_BC_ANTIPERIODIC_T && fmt != GF_FULL) ? 1 : 0;
+  A.t_off = geo.coords[0] * geo.local[0];
+  A.bc_tlast = geo.global[0] - 1;
   const bool reduce = c.epi != EPI_STORE;
   cudaStream_t s = ctx->stream;
 
@@ -409,16 +408,13 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     A.nsites = static_cast<int>(geo.vh);
     A.both = npar == 2;
     A.par0 = pars[0];
-    int blocks = 0;
-    dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-      blocks = hop_blocks<decltype(Dc)::value, decltype(Rc)::value>(A.nsites, npar);
-    });
+    const int blocks = hop_blocks(A.nsites, npar);
     if (reduce) {
       if (blocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
       A.red = Reduce{ctx->partials, ctx->ticket, c.result, 0, blocks};
     }
-    dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(A, false, c.epi, A.nsites, npar, s);
+    dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaGetLastError());
@@ -427,18 +423,16 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
 
   // ---- decomposed: pack -> exchange -> interior -> boundary -------------
   HaloBufs& hb = halo_bufs(ctx, dr);
-  int total_blocks = 0, bnd_off[2] = {0, 0}, int_blocks[2] = {0, 0}, bnd_blocks[2] = {0, 0};
+  int total_blocks = 0, int_blocks[2] = {0, 0}, bnd_blocks[2] = {0, 0};
   for (int k = 0; k < npar; ++k) {
     const int p = pars[k];
-    dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-      int_blocks[k] = hop_blocks<decltype(Dc)::value, decltype(Rc)::value>(ctx->nint[p], 1);
-      bnd_blocks[k] = hop_blocks<decltype(Dc)::value, decltype(Rc)::value>(ctx->nbnd[p], 1);
-    });
+    int_blocks[k] = hop_blocks(ctx->nint[p], 1);
+    bnd_blocks[k] = hop_blocks(ctx->nbnd[p], 1);
     total_blocks += int_blocks[k] + bnd_blocks[k];
   }
   if (reduce && total_blocks > ctx->max_partials)
     throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
-  // the exchange for one output parity at a time keeps message buffers simple
+  // one exchange per output parity keeps the message buffers simple
   for (int k = 0; k < npar; ++k) {
     const int p = pars[k], q = p ^ 1;
     std::vector<Transport::Msg> msgs;
@@ -453,9 +447,12 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       P.dir = f % 2;
       P.count = static_cast<int>(ctx->plan.count[f]);
       P.s5in = c.s5in;
+      P.bc_kernel = A.bc_kernel;
+      P.t_off = A.t_off;
+      P.bc_tlast = A.bc_tlast;
       P.outbuf = hb.send[f];
-      dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-        launch_pack<decltype(Dc)::value, decltype(Rc)::value>(P, s);
+      dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
+        pack_kernel<LBCU_TPARAMS(Dc, Rc, Fc)><<<(P.count + kBlock - 1) / kBlock, kBlock, 0, s>>>(P);
       });
       ctx->launches += 1;
       // face f goes to partner[f]; the matching halo arrives from the opposite
@@ -480,8 +477,8 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     for (int kk = 0; kk < k; ++kk) off += int_blocks[kk] + bnd_blocks[kk];
     if (reduce) Ai.red = Reduce{ctx->partials, ctx->ticket, c.result, off, total_blocks};
     LBCU_CUDA(cudaEventRecord(ctx->ev_pack, s));
-    dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(Ai, false, c.epi, Ai.nsites, 1, s);
+    dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ai, false, c.epi, Ai.nsites, 1, s);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_pack, 0));
@@ -498,10 +495,9 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       Ab.hbwd[mu] = hb.recv[2 * mu + 0];
       Ab.hcount[mu] = static_cast<int>(ctx->plan.count[2 * mu]);
     }
-    bnd_off[k] = off + int_blocks[k];
-    if (reduce) Ab.red = Reduce{ctx->partials, ctx->ticket, c.result, bnd_off[k], total_blocks};
-    dispatch_rep(dr, real, [&](auto Dc, auto Rc) {
-      launch_hop<decltype(Dc)::value, decltype(Rc)::value>(Ab, true, c.epi, Ab.nsites, 1, s);
+    if (reduce) Ab.red = Reduce{ctx->partials, ctx->ticket, c.result, off + int_blocks[k], total_blocks};
+    dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ab, true, c.epi, Ab.nsites, 1, s);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaGetLastError());

@@ -1,0 +1,147 @@
+// Gauge-link storage formats and the link x half-spinor multiply (sm_100a).
+//
+// The reference stores every represented link as a dense dr x dr complex (or
+// real, adjoint) matrix (proj/include/latbench/fields.hpp:37-57). Links are
+// 67-86 % of the Dslash's compulsory HBM traffic, so the device keeps them in
+// the most compact exact form the group structure allows and rebuilds the
+// represented matrix in registers (fp64 FMAs are nearly free in this
+// HBM-bound kernel):
+//
+//   GF_FULL : dense dr x dr (any representation), antiperiodic sign baked in
+//   GF_SU2  : SU(2) element U = [[al, be], [-conj(be), conj(al)]], 2 complex:
+//             fundamental (dr = 2) directly; adjoint (dr = 3, real) through
+//             R_ab = 1/2 tr(s_a U s_b U^dag) = (a0^2 - |a|^2) d_ab + 2 a_a a_b
+//             - 2 a0 eps_abc a_c with al = a0 + i a3, be = a2 + i a1
+//             (group.cpp:126-143 convention, checked in tests/test_host.py)
+//   GF_R12  : SU(3) rows 0 and 1 (6 complex); row 2 = conj(row0 x row1)
+//
+// Compact formats are chosen at upload only when every link reconstructs to
+// within 1e-12 of the uploaded matrix (gauge.cu), so arbitrary user links
+// (non-unitary, tampered) stay exact in GF_FULL. In compact formats the
+// antiperiodic time sign is applied in the kernel instead of being baked in
+// (a baked -U would break det U = 1 for SU(3)).
+#pragma once
+
+#include <type_traits>
+
+#include "device.cuh"
+
+namespace lbcu {
+
+enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2 };
+
+template <bool REAL>
+using LinkT = std::conditional_t<REAL, double, double2>;
+
+template <int D, bool REAL, int FMT>
+struct LinkFmt {
+  static constexpr bool valid = FMT == GF_FULL || (FMT == GF_SU2 && ((D == 2 && !REAL) || (D == 3 && REAL))) ||
+                                (FMT == GF_R12 && D == 3 && !REAL);
+  static constexpr int entries = FMT == GF_FULL ? D * D : (FMT == GF_SU2 ? 2 : 6);
+  using Elem = std::conditional_t<FMT == GF_FULL, LinkT<REAL>, double2>;
+};
+
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+// Rebuild the represented link (row-major D x D) from compact entries.
+template <int D, bool REAL, int FMT>
+__device__ __forceinline__ void build_link(LinkT<REAL> (&u)[D * D],
+                                           const double2 (&s)[LinkFmt<D, REAL, FMT>::entries]) {
+  static_assert(FMT != GF_FULL, "dense links need no rebuild");
+  if constexpr (FMT == GF_SU2 && !REAL) {
+    const double2 al = s[0], be = s[1];
+    u[0] = al;
+    u[1] = be;
+    u[2] = make_double2(-be.x, be.y);
+    u[3] = cconj(al);
+  } else if constexpr (FMT == GF_SU2 && REAL) {
+    const double2 al = s[0], be = s[1];
+    const double a0 = al.x, a3 = al.y, a2 = be.x, a1 = be.y;
+    const double d = a0 * a0 - (a1 * a1 + a2 * a2 + a3 * a3);
+    const double t1 = 2.0 * a1, t2 = 2.0 * a2, t3 = 2.0 * a3, w = 2.0 * a0;
+    u[0] = fma(t1, a1, d);
+    u[1] = fma(t1, a2, w * a3);
+    u[2] = fma(t1, a3, -w * a2);
+    u[3] = fma(t2, a1, -w * a3);
+    u[4] = fma(t2, a2, d);
+    u[5] = fma(t2, a3, w * a1);
+    u[6] = fma(t3, a1, w * a2);
+    u[7] = fma(t3, a2, -w * a1);
+    u[8] = fma(t3, a3, d);
+  } else {  // GF_R12
+#pragma unroll
+    for (int e = 0; e < 6; ++e) u[e] = s[e];
+    u[6] = cconj(csub(cmul(u[1], u[5]), cmul(u[2], u[4])));
+    u[7] = cconj(csub(cmul(u[2], u[3]), cmul(u[0], u[5])));
+    u[8] = cconj(csub(cmul(u[0], u[4]), cmul(u[1], u[3])));
+  }
+}
+
+// Load a link from its storage (read-only path) and rebuild it.
+template <int D, bool REAL, int FMT>
+__device__ __forceinline__ void load_link(LinkT<REAL> (&u)[D * D],
+                                          const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
+                                          long long st) {
+  if constexpr (FMT == GF_FULL) {
+#pragma unroll
+    for (int e = 0; e < D * D; ++e) u[e] = __ldg(p + (long long)e * st);
+  } else {
+    double2 s[LinkFmt<D, REAL, FMT>::entries];
+#pragma unroll
+    for (int e = 0; e < LinkFmt<D, REAL, FMT>::entries; ++e) s[e] = __ldg(p + (long long)e * st);
+    build_link<D, REAL, FMT>(u, s);
+  }
+}
+
+// g[a][r] = sum_c M_rc h[a][c] with M = U (DAG = false) or U^dag (DAG = true)
+template <int D, bool REAL, int FMT, bool DAG>
+__device__ __forceinline__ void link_mul(double2 (&g)[2][D],
+                                         const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
+                                         long long st, const double2 (&h)[2][D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r) g[0][r] = g[1][r] = make_double2(0.0, 0.0);
+  if constexpr (FMT == GF_FULL) {
+    // stream the entries: no need to hold the whole matrix in registers
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const auto u = __ldg(p + (long long)(DAG ? c * D + r : r * D + c) * st);
+        if constexpr (REAL) {
+          rmac(g[0][r], u, h[0][c]);
+          rmac(g[1][r], u, h[1][c]);
+        } else if constexpr (DAG) {
+          cmac_conj(g[0][r], u, h[0][c]);
+          cmac_conj(g[1][r], u, h[1][c]);
+        } else {
+          cmac(g[0][r], u, h[0][c]);
+          cmac(g[1][r], u, h[1][c]);
+        }
+      }
+  } else {
+    LinkT<REAL> u[D * D];
+    load_link<D, REAL, FMT>(u, p, st);
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const auto e = u[DAG ? c * D + r : r * D + c];
+        if constexpr (REAL) {
+          rmac(g[0][r], e, h[0][c]);
+          rmac(g[1][r], e, h[1][c]);
+        } else if constexpr (DAG) {
+          cmac_conj(g[0][r], e, h[0][c]);
+          cmac_conj(g[1][r], e, h[1][c]);
+        } else {
+          cmac(g[0][r], e, h[0][c]);
+          cmac(g[1][r], e, h[1][c]);
+        }
+      }
+  }
+}
+
+}  // namespace lbcu

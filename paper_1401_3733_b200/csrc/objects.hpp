@@ -25,8 +25,13 @@ struct lbcu_gauge_s {
   lbcu_ctx_s* ctx = nullptr;
   int n = 0, rep = 0, dr = 0, bc = 0;
   bool real = false;
-  void* base = nullptr;  // [2 parity][4 mu][dr][dr][stride] of double2 (complex) or double
-  size_t bytes = 0;
+  // [2 parity][4 mu][entries][stride]: GF_FULL dense dr x dr (double2, or
+  // double for real links, BC sign baked in); compact formats (links.cuh)
+  // store double2 entries and apply the BC sign in the kernels
+  void* base = nullptr;
+  int fmt = 0;
+  bool compact_ok = true;     // lbcu_gauge_set_compact
+  double compact_err = -1.0;  // max reconstruction error seen at the last upload
 };
 
 namespace lbcu {

@@ -274,3 +274,47 @@ def test_near_unit_links_cg_eo():
     ref = O.ref_cg_eo(L, [1, 1, 1, 1], n, rep, 1, 0.02, g, s, 1e-12)
     assert abs(o.iterations - ref["iterations"]) <= 1
     assert o.true_rel_residual < 2e-12
+
+
+@pytest.mark.parametrize("n,rep,links,fmt", [
+    (2, lb.FUNDAMENTAL, lb.LINKS_HAAR, "su2"),
+    (2, lb.ADJOINT, lb.LINKS_HAAR, "su2"),
+    (3, lb.FUNDAMENTAL, lb.LINKS_HAAR, "r12"),
+    (3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT, "r12"),
+    (4, lb.ANTISYMMETRIC, lb.LINKS_HAAR, "full"),
+], ids=["su2f", "su2a", "su3f", "su3f-near-unit", "su4as"])
+@pytest.mark.parametrize("bc", [lb.PERIODIC, lb.ANTIPERIODIC_T], ids=["periodic", "antiperiodic"])
+def test_compact_link_storage_is_exact(n, rep, links, fmt, bc):
+    """Compact link formats (links.cuh) give the same Dphi as dense storage and
+    the oracle, and download the uploaded links."""
+    L = [4, 4, 6, 4]
+    dr, g, s = fields(L, n, rep, links=links)
+    ctx = lb.Context(L)
+    gc = lb.GaugeField(ctx, n, rep, bc).upload(g)
+    gf = lb.GaugeField(ctx, n, rep, bc).set_compact(False).upload(g)
+    assert gc.storage()[0] == fmt and gf.storage()[0] == "full"
+    if fmt != "full":
+        assert gc.storage()[1] < 1e-13
+    inp = lb.SpinorField(ctx, dr).upload(s)
+    oc, of = lb.SpinorField(ctx, dr), lb.SpinorField(ctx, dr)
+    lb.apply_dirac(oc, gc, inp, 0.1)
+    lb.apply_dirac(of, gf, inp, 0.1)
+    want = O.port_dirac(L, bc, 0.1, g, s)
+    assert rel_l2(oc.download(), want) < TOL_DPHI
+    assert rel_l2(of.download(), want) < TOL_DPHI
+    assert np.abs(gc.download() - g).max() < 1e-12
+    assert np.array_equal(gf.download(), g)
+
+
+def test_non_group_links_stay_dense():
+    """Arbitrary (non-unitary) links must not be compressed."""
+    L = [4, 4, 4, 4]
+    rng = np.random.default_rng(3)
+    g = rng.normal(size=(256, 4, 3, 3)) + 1j * rng.normal(size=(256, 4, 3, 3))
+    s = lb.init_spinor_random(L, 3, 1, 0)
+    ctx = lb.Context(L)
+    gauge = lb.GaugeField(ctx, 3, lb.FUNDAMENTAL, lb.ANTIPERIODIC_T).upload(g)
+    assert gauge.storage()[0] == "full"
+    inp, out = lb.SpinorField(ctx, 3).upload(s), lb.SpinorField(ctx, 3)
+    lb.apply_dirac(out, gauge, inp, 0.1)
+    assert rel_l2(out.download(), O.port_dirac(L, 1, 0.1, g, s)) < TOL_DPHI

@@ -21,7 +21,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--minb", default="1,3,4,5,6,8")
+    ap.add_argument("--minb", default="1,3")
+    ap.add_argument("--compact", default="0,1")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     L, n, rep, mass = cfg["L"], cfg["n"], cfg["rep"], cfg["mass"]
@@ -29,7 +30,8 @@ def main():
     real = lb.rep_is_real(rep)
     links = {"haar": lb.LINKS_HAAR, "near_unit": lb.LINKS_NEAR_UNIT}[cfg["links"]]
     ctx = lb.Context(L)
-    gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(lb.init_gauge_random(L, n, rep, 1, links=links))
+    links_host = lb.init_gauge_random(L, n, rep, 1, links=links)
+    gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T)
     s = lb.init_spinor_random(L, dr, 1, 0)
     a = lb.SpinorField(ctx, dr).upload(s)
     b = lb.SpinorField(ctx, dr)
@@ -40,7 +42,11 @@ def main():
     bhop = (128 * dr + 64 * (1 if real else 2) * dr * dr) * V / 2
     ref = None
     res = []
-    for mb in [int(x) for x in args.minb.split(",")]:
+    for cp in [int(x) for x in args.compact.split(",")]:
+      os.environ["LBCU_GAUGE_COMPACT"] = str(cp)
+      gauge.upload(links_host)
+      fmt = gauge.storage()
+      for mb in [int(x) for x in args.minb.split(",")]:
         if True:
             os.environ["LBCU_HOP_MINB"] = str(mb)
             try:
@@ -63,7 +69,7 @@ def main():
                 if ref is None:
                     ref = out
                 err = float(np.linalg.norm(out - ref) / np.linalg.norm(ref))
-                r = dict(minb=mb, full_ms=t_full, full_gbs=bfull / t_full / 1e6,
+                r = dict(compact=cp, fmt=fmt, minb=mb, full_ms=t_full, full_gbs=bfull / t_full / 1e6,
                          hop_ms=t_hop, hop_gbs=bhop / t_hop / 1e6, err=err)
             except Exception as e:  # noqa: BLE001
                 r = dict(minb=mb, error=str(e))
