@@ -100,6 +100,33 @@ __device__ __forceinline__ const ElemT<D, REAL, FMT>* link_ptr(const void* gauge
   return static_cast<const ElemT<D, REAL, FMT>*>(gauge) + (long long)(par * 4 + mu) * E * st + site;
 }
 
+// Multiply by the link and reconstruct into acc. Small dr: row-fused (no
+// intermediate g); large dr: the two-phase form schedules better.
+template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
+__device__ __forceinline__ void link_hop(double2 (&acc)[4][D], const ElemT<D, REAL, FMT>* p,
+                                         long long st, const double2 (&h)[2][D]) {
+  if constexpr (D <= 3) {
+    link_mul_acc<D, REAL, FMT, DAG, R0, R1, Q0, Q1>(acc, p, st, h);
+  } else {
+    double2 g[2][D];
+    link_mul<D, REAL, FMT, DAG>(g, p, st, h);
+    reconstruct<D, R0, R1, Q0, Q1>(acc, g);
+  }
+}
+
+// Antiperiodic-t sign of a compact link (dense links carry it baked in):
+// branch-free so the scheduler can still hoist the next direction's loads.
+template <int D, int FMT>
+__device__ __forceinline__ void bc_sign(double2 (&h)[2][D], bool flip) {
+  if constexpr (FMT != GF_FULL) {
+    const double sg = flip ? -1.0 : 1.0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < D; ++c) h[a][c] = cscale(sg, h[a][c]);
+  }
+}
+
 template <int D, bool REAL, int FMT, bool BND, int MU>
 __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
                                        const double2* __restrict__ in, int par, int i, int s,
@@ -107,7 +134,7 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
   using G = Gam<MU>;
   const long long st = A.g.stride;
   {  // forward: (1 - g_mu) U_mu(x) in(x + mu)
-    double2 h[2][D], g[2][D];
+    double2 h[2][D];
     if (BND && !A.g.wrap[MU] && c[MU] == A.g.L[MU] - 1) {
       const int j = face_pos(A.g, c, MU) >> 1;
       const int hc = A.hcount[MU];
@@ -118,30 +145,31 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
     } else {
       project<D, G::p0, G::p1, G::f0, G::f1>(h, in, st, nb_fwd(A.g, s, c, MU) >> 1, A.s5in);
     }
-    if (MU == 0 && A.bc_kernel && A.t_off + c[0] == A.bc_tlast) negate<D>(h);
-    link_mul<D, REAL, FMT, false>(g, link_ptr<D, REAL, FMT>(A.gauge, st, par, MU, i), st, h);
-    reconstruct<D, G::r0, G::r1, G::q0, G::q1>(acc, g);
+    if constexpr (MU == 0) bc_sign<D, FMT>(h, A.bc_kernel && A.t_off + c[0] == A.bc_tlast);
+    link_hop<D, REAL, FMT, false, G::r0, G::r1, G::q0, G::q1>(
+        acc, link_ptr<D, REAL, FMT>(A.gauge, st, par, MU, i), st, h);
   }
   {  // backward: (1 + g_mu) U_mu(x - mu)^dag in(x - mu)
-    double2 g[2][D];
     if (BND && !A.g.wrap[MU] && c[MU] == 0) {
+      double2 g[2][D];
       const int j = face_pos(A.g, c, MU) >> 1;
       const int hc = A.hcount[MU];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int cc = 0; cc < D; ++cc) g[a][cc] = ldg(A.hbwd[MU] + (a * D + cc) * hc + j);
+      reconstruct<D, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, g);
     } else {
       double2 h[2][D];
       const int nb = nb_bwd(A.g, s, c, MU) >> 1;
       project<D, G::p0, G::p1, G::f0 ^ 1, G::f1 ^ 1>(h, in, st, nb, A.s5in);
-      if (MU == 0 && A.bc_kernel) {
+      if constexpr (MU == 0) {
         const int tl = c[0] > 0 ? c[0] - 1 : A.g.L[0] - 1;
-        if (A.t_off + tl == A.bc_tlast) negate<D>(h);
+        bc_sign<D, FMT>(h, A.bc_kernel && A.t_off + tl == A.bc_tlast);
       }
-      link_mul<D, REAL, FMT, true>(g, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, MU, nb), st, h);
+      link_hop<D, REAL, FMT, true, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(
+          acc, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, MU, nb), st, h);
     }
-    reconstruct<D, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, g);
   }
 }
 
@@ -287,7 +315,7 @@ int default_minb() {
   return 1;
 }
 
-int hop_blocks(int nsites, int npar) { return (nsites + kBlock - 1) / kBlock * npar; }
+int hop_blocks(int nsites, int npar, int /*dr*/) { return (nsites + kBlock - 1) / kBlock * npar; }
 
 template <int D, bool REAL, int FMT, int MINB>
 void launch_hop_minb(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream_t s) {
@@ -308,7 +336,7 @@ void launch_hop_minb(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream
 template <int D, bool REAL, int FMT>
 void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaStream_t s) {
   if (nsites <= 0) return;
-  const int blocks = hop_blocks(nsites, npar);
+  const int blocks = hop_blocks(nsites, npar, D);
   if constexpr (D <= 3) {
     if (env_int("LBCU_HOP_MINB", default_minb<D, REAL, FMT>()) == 3) {
       launch_hop_minb<D, REAL, FMT, 3>(A, bnd, epi, blocks, s);
@@ -408,7 +436,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     A.nsites = static_cast<int>(geo.vh);
     A.both = npar == 2;
     A.par0 = pars[0];
-    const int blocks = hop_blocks(A.nsites, npar);
+    const int blocks = hop_blocks(A.nsites, npar, dr);
     if (reduce) {
       if (blocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
       A.red = Reduce{ctx->partials, ctx->ticket, c.result, 0, blocks};
@@ -426,8 +454,8 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   int total_blocks = 0, int_blocks[2] = {0, 0}, bnd_blocks[2] = {0, 0};
   for (int k = 0; k < npar; ++k) {
     const int p = pars[k];
-    int_blocks[k] = hop_blocks(ctx->nint[p], 1);
-    bnd_blocks[k] = hop_blocks(ctx->nbnd[p], 1);
+    int_blocks[k] = hop_blocks(ctx->nint[p], 1, dr);
+    bnd_blocks[k] = hop_blocks(ctx->nbnd[p], 1, dr);
     total_blocks += int_blocks[k] + bnd_blocks[k];
   }
   if (reduce && total_blocks > ctx->max_partials)

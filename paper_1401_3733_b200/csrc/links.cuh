@@ -144,4 +144,41 @@ __device__ __forceinline__ void link_mul(double2 (&g)[2][D],
   }
 }
 
+// Row-fused multiply + spin reconstruction: for each colour row r,
+//   g_a = sum_c M_rc h[a][c]  (a = 0, 1), then
+//   acc[0][r] += g_0; acc[1][r] += g_1; acc[2][r] += Q0 g_R0; acc[3][r] += Q1 g_R1
+// so the 2 x D intermediate g never has to be held in registers.
+template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
+__device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
+                                             const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
+                                             long long st, const double2 (&h)[2][D]) {
+  [[maybe_unused]] LinkT<REAL> u[FMT == GF_FULL ? 1 : D * D];
+  if constexpr (FMT != GF_FULL) load_link<D, REAL, FMT>(u, p, st);
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    double2 g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const int idx = DAG ? c * D + r : r * D + c;
+      LinkT<REAL> e;
+      if constexpr (FMT == GF_FULL) e = __ldg(p + (long long)idx * st);
+      else e = u[idx];
+      if constexpr (REAL) {
+        rmac(g0, e, h[0][c]);
+        rmac(g1, e, h[1][c]);
+      } else if constexpr (DAG) {
+        cmac_conj(g0, e, h[0][c]);
+        cmac_conj(g1, e, h[1][c]);
+      } else {
+        cmac(g0, e, h[0][c]);
+        cmac(g1, e, h[1][c]);
+      }
+    }
+    acc[0][r] = cadd(acc[0][r], g0);
+    acc[1][r] = cadd(acc[1][r], g1);
+    acc[2][r] = cadd(acc[2][r], phm<Q0>(R0 == 0 ? g0 : g1));
+    acc[3][r] = cadd(acc[3][r], phm<Q1>(R1 == 0 ? g0 : g1));
+  }
+}
+
 }  // namespace lbcu

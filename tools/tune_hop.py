@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--minb", default="1,3")
     ap.add_argument("--compact", default="0,1")
+    ap.add_argument("--s2", default=None, help="LBCU_HOP_S2 values to sweep (spin-split kernel)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     L, n, rep, mass = cfg["L"], cfg["n"], cfg["rep"], cfg["mass"]
@@ -46,9 +47,13 @@ def main():
       os.environ["LBCU_GAUGE_COMPACT"] = str(cp)
       gauge.upload(links_host)
       fmt = gauge.storage()
-      for mb in [int(x) for x in args.minb.split(",")]:
+      sweep = [(mb, s2) for mb in [int(x) for x in args.minb.split(",")]
+               for s2 in ([int(x) for x in args.s2.split(",")] if args.s2 else [None])]
+      for mb, s2 in sweep:
         if True:
             os.environ["LBCU_HOP_MINB"] = str(mb)
+            if s2 is not None:
+                os.environ["LBCU_HOP_S2"] = str(s2)
             try:
                 for _ in range(3):
                     lb.apply_dirac(b, gauge, a, mass)
@@ -69,7 +74,7 @@ def main():
                 if ref is None:
                     ref = out
                 err = float(np.linalg.norm(out - ref) / np.linalg.norm(ref))
-                r = dict(compact=cp, fmt=fmt, minb=mb, full_ms=t_full, full_gbs=bfull / t_full / 1e6,
+                r = dict(compact=cp, fmt=fmt, minb=mb, s2=s2, full_ms=t_full, full_gbs=bfull / t_full / 1e6,
                          hop_ms=t_hop, hop_gbs=bhop / t_hop / 1e6, err=err)
             except Exception as e:  # noqa: BLE001
                 r = dict(minb=mb, error=str(e))
