@@ -123,6 +123,8 @@ int lbcu_ctx_synchronize(lbcu_ctx c);
 void* lbcu_ctx_stream(lbcu_ctx c); /* the cudaStream_t all work is issued on */
 int lbcu_ctx_local(lbcu_ctx c, int local[4]);
 int lbcu_barrier(lbcu_ctx c);      /* Worker::barrier, transport.cpp:79 */
+/* Worker::global_sum of host values (transport.cpp:83-100), in place, collective */
+int lbcu_allreduce_sum(lbcu_ctx c, double* values, int n);
 /* launches of library kernels issued on this context since creation */
 long long lbcu_ctx_kernel_launches(lbcu_ctx c);
 /* CUDA-event timing on the context stream (slot 0..15) */
@@ -141,8 +143,19 @@ int lbcu_gauge_download(lbcu_gauge g, double* host); /* as uploaded (no BC sign)
  *   LBCU_GAUGE_R12 : SU(3) fundamental, two rows (third = conj(r0 x r1))
  * otherwise LBCU_GAUGE_FULL (dense dr x dr). set_compact(0) before upload
  * forces dense storage. */
-enum lbcu_gauge_format { LBCU_GAUGE_FULL = 0, LBCU_GAUGE_SU2 = 1, LBCU_GAUGE_R12 = 2 };
+enum lbcu_gauge_format {
+  LBCU_GAUGE_FULL = 0,
+  LBCU_GAUGE_SU2 = 1,
+  LBCU_GAUGE_R12 = 2,
+  LBCU_GAUGE_AS4 = 3 /* SU(4) antisymmetric formed from fundamental links */
+};
 int lbcu_gauge_set_compact(lbcu_gauge g, int enable);
+/* Upload the FUNDAMENTAL SU(N) links (host layout [site][mu][N][N] complex,
+ * the group elements randomize_gauge_interior draws before represent(),
+ * fields.cpp:95-96); the represented link is formed on the fly in the
+ * kernels. Supported for the SU(4) antisymmetric representation (BASELINE
+ * config 5): 16 instead of 36 complex numbers per link. */
+int lbcu_gauge_upload_fundamental(lbcu_gauge g, const double* host_fundamental);
 int lbcu_gauge_storage(lbcu_gauge g, int* format, double* reconstruction_error);
 int lbcu_gauge_destroy(lbcu_gauge g);
 
@@ -158,6 +171,12 @@ int lbcu_spinor_destroy(lbcu_spinor s);
 /* ---- operators (collective; each performs its own halo exchange) --------- */
 /* apply_dirac, kernels.hpp:19-20: out = (4+m) in - 1/2 sum_mu hops. FULL fields. */
 int lbcu_dphi(lbcu_spinor out, lbcu_gauge g, lbcu_spinor in, double mass);
+/* apply_dirac on HOST fields (reference interior layout): out[k] = D in[k]
+ * for k < nfields, with the host->device copy of field k+1 and the
+ * device->host copy of field k-1 overlapped with the kernels of field k.
+ * Pinned host buffers run at full PCIe duplex. Blocks until all are done. */
+int lbcu_dphi_host(lbcu_gauge g, double mass, int nfields, const double* const* in,
+                   double* const* out);
 /* gamma5 . apply_dirac, as composed in apply_h (solver.cpp:11-12) */
 int lbcu_g5dphi(lbcu_spinor out, lbcu_gauge g, lbcu_spinor in, double mass);
 /* even-odd blocks of D (no reference analogue):

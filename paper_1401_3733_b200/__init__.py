@@ -144,6 +144,7 @@ def lib():
             "lbcu_gauge_download": (C.c_int, [_vp, _dp]),
             "lbcu_gauge_destroy": (C.c_int, [_vp]),
             "lbcu_gauge_set_compact": (C.c_int, [_vp, C.c_int]),
+            "lbcu_gauge_upload_fundamental": (C.c_int, [_vp, _dp]),
             "lbcu_gauge_storage": (C.c_int, [_vp, _ip, _dp]),
             "lbcu_spinor_create": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
             "lbcu_spinor_upload": (C.c_int, [_vp, _dp]),
@@ -151,6 +152,8 @@ def lib():
             "lbcu_spinor_subset": (C.c_int, [_vp]),
             "lbcu_spinor_destroy": (C.c_int, [_vp]),
             "lbcu_dphi": (C.c_int, [_vp, _vp, _vp, C.c_double]),
+            "lbcu_dphi_host": (C.c_int, [_vp, C.c_double, C.c_int, C.POINTER(_dp), C.POINTER(_dp)]),
+            "lbcu_allreduce_sum": (C.c_int, [_vp, _dp, C.c_int]),
             "lbcu_g5dphi": (C.c_int, [_vp, _vp, _vp, C.c_double]),
             "lbcu_dphi_eo": (C.c_int, [_vp, _vp, _vp]),
             "lbcu_dphi_oe": (C.c_int, [_vp, _vp, _vp]),
@@ -376,6 +379,15 @@ class GaugeField:
         _check(lib().lbcu_gauge_upload(self._h, a.ctypes.data_as(_dp)))
         return self
 
+    def upload_fundamental(self, links: np.ndarray):
+        """Upload the fundamental SU(N) links ([V, 4, N, N] complex); the
+        representation is formed in the kernels (SU(4) antisymmetric)."""
+        a = np.ascontiguousarray(links, dtype=np.complex128)
+        if a.size != self.ctx.volume * 4 * self.group_rank ** 2:
+            raise ContractViolation("fundamental upload expects [V, 4, N, N] complex")
+        _check(lib().lbcu_gauge_upload_fundamental(self._h, a.ctypes.data_as(_dp)))
+        return self
+
     def set_compact(self, enable: bool):
         """Allow (default) or forbid compact link storage for later uploads."""
         _check(lib().lbcu_gauge_set_compact(self._h, int(bool(enable))))
@@ -385,7 +397,7 @@ class GaugeField:
         """(format name, max reconstruction error at the last upload)."""
         f, e = C.c_int(), C.c_double()
         _check(lib().lbcu_gauge_storage(self._h, C.byref(f), C.byref(e)))
-        return {0: "full", 1: "su2", 2: "r12"}[f.value], e.value
+        return {0: "full", 1: "su2", 2: "r12", 3: "as4"}[f.value], e.value
 
     def download(self) -> np.ndarray:
         dt = np.float64 if self.real_links else np.complex128
@@ -442,6 +454,17 @@ class SpinorField:
 def apply_dirac(out: SpinorField, gauge: GaugeField, in_: SpinorField, mass: float):
     """kernels.hpp:19-20 — out = (4+m) in - 1/2 sum_mu hops."""
     _check(lib().lbcu_dphi(out._h, gauge._h, in_._h, float(mass)))
+
+
+def dphi_host(gauge: GaugeField, mass: float, ins: Sequence[int], outs: Sequence[int]):
+    """apply_dirac on host fields (addresses of reference-layout buffers):
+    outs[k] = D ins[k], transfers overlapped with the kernels."""
+    n = len(ins)
+    if len(outs) != n:
+        raise ContractViolation("dphi_host: ins and outs differ in length")
+    ia = (_dp * n)(*[C.cast(C.c_void_p(int(p)), _dp) for p in ins])
+    oa = (_dp * n)(*[C.cast(C.c_void_p(int(p)), _dp) for p in outs])
+    _check(lib().lbcu_dphi_host(gauge._h, float(mass), n, ia, oa))
 
 
 def apply_g5dirac(out, gauge, in_, mass):

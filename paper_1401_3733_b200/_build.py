@@ -56,10 +56,30 @@ def _compile(src, verbose):
     return obj
 
 
+DRIVER_SRC = os.path.join(ROOT, "tools", "latbench_b200.cpp")
+DRIVER = os.path.join(ROOT, "tools", "latbench_b200")
+
+
+def build_driver() -> str:
+    """The C++ benchmark driver (run_suite on the device path) over liblbcu.so."""
+    deps = [DRIVER_SRC, LIB, os.path.join(ROOT, "include", "latbench_b200.hpp"),
+            os.path.join(ROOT, "include", "lbcu.h")]
+    if not _newer(DRIVER, deps):
+        return DRIVER
+    cmd = [os.environ.get("CXX_DRIVER", "g++"), "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+           DRIVER_SRC, "-o", DRIVER, "-L", PKG, "-llbcu", "-Wl,-rpath,$ORIGIN/../paper_1401_3733_b200",
+           "-lpthread"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"driver build failed:\n{r.stderr}")
+    return DRIVER
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
     if not force and not _newer(LIB, [*srcs, *_headers(), __file__]):
+        build_driver()
         return LIB  # up to date (the GPU box receives the library without build/)
     if force:
         for s in srcs:
@@ -73,6 +93,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    build_driver()
     return LIB
 
 

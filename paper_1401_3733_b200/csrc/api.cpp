@@ -308,6 +308,7 @@ int lbcu_ctx_destroy(lbcu_ctx c) {
   if (!c) return LBCU_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  host_pipe_release(c);
   for (auto& kv : c->scratch) free_spinor(kv.second);
   for (auto& kv : c->halo)
     for (int f = 0; f < 8; ++f) {
@@ -356,6 +357,18 @@ int lbcu_barrier(lbcu_ctx c) {
   bind(c);
   LBCU_CUDA(cudaStreamSynchronize(c->stream));
   c->world->t->barrier(c->rank);
+  API_END
+}
+
+int lbcu_allreduce_sum(lbcu_ctx c, double* values, int n) {
+  API_BEGIN
+  need(c && values && n >= 1 && n <= 16, "allreduce_sum: 1..16 values");
+  bind(c);
+  double* d = c->dscal + 40;
+  LBCU_CUDA(cudaMemcpyAsync(d, values, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  c->world->t->allreduce(c->rank, d, n, c->stream);
+  LBCU_CUDA(cudaMemcpyAsync(values, d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LBCU_CUDA(cudaStreamSynchronize(c->stream));
   API_END
 }
 
@@ -414,6 +427,14 @@ int lbcu_gauge_download(lbcu_gauge g, double* host) {
   need(g && host, "lbcu_gauge_download: null argument");
   bind(g->ctx);
   gauge_download(g->ctx, g, host);
+  API_END
+}
+
+int lbcu_gauge_upload_fundamental(lbcu_gauge g, const double* host) {
+  API_BEGIN
+  need(g && host, "lbcu_gauge_upload_fundamental: null argument");
+  bind(g->ctx);
+  gauge_upload_fundamental(g->ctx, g, host);
   API_END
 }
 
@@ -493,6 +514,16 @@ int lbcu_dphi(lbcu_spinor out, lbcu_gauge g, lbcu_spinor in, double mass) {
   hc.a = 4.0 + mass;
   hc.b = -0.5;
   hop_apply(in->ctx, hc);
+  API_END
+}
+
+int lbcu_dphi_host(lbcu_gauge g, double mass, int nfields, const double* const* in,
+                   double* const* out) {
+  API_BEGIN
+  need(g && in && out && nfields >= 0, "dphi_host: null argument");
+  for (int k = 0; k < nfields; ++k) need(in[k] && out[k], "dphi_host: null field buffer");
+  bind(g->ctx);
+  dphi_host_batch(g->ctx, g, mass, nfields, in, out);
   API_END
 }
 

@@ -357,6 +357,85 @@ void spinor_upload(lbcu_ctx_s* ctx, lbcu_spinor_s* s, const double* host) {
   LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// Host-field Dphi with copy/compute overlap: field k's host->device copy runs
+// on pipe.h2d while field k-1 is transposed and multiplied on the compute
+// stream and field k-2's result returns on pipe.d2h (two device slots, events
+// order the reuse of each slot). Pinned host buffers give full PCIe duplex.
+void dphi_host_batch(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double mass, int n,
+                     const double* const* in, double* const* out) {
+  auto& P = ctx->pipe;
+  const int dr = g->dr, nv = 4 * dr;
+  const size_t bytes = static_cast<size_t>(ctx->geo.volume) * nv * sizeof(double2);
+  if (!P.h2d) {
+    LBCU_CUDA(cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking));
+    LBCU_CUDA(cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking));
+    for (int s = 0; s < 2; ++s) {
+      LBCU_CUDA(cudaEventCreateWithFlags(&P.ev_h2d[s], cudaEventDisableTiming));
+      LBCU_CUDA(cudaEventCreateWithFlags(&P.ev_in_free[s], cudaEventDisableTiming));
+      LBCU_CUDA(cudaEventCreateWithFlags(&P.ev_out[s], cudaEventDisableTiming));
+      LBCU_CUDA(cudaEventCreateWithFlags(&P.ev_d2h[s], cudaEventDisableTiming));
+    }
+  }
+  if (P.bytes < bytes) {
+    for (int s = 0; s < 2; ++s) {
+      if (P.stage_in[s]) LBCU_CUDA(cudaFree(P.stage_in[s]));
+      if (P.stage_out[s]) LBCU_CUDA(cudaFree(P.stage_out[s]));
+      LBCU_CUDA(cudaMalloc(&P.stage_in[s], bytes));
+      LBCU_CUDA(cudaMalloc(&P.stage_out[s], bytes));
+    }
+    P.bytes = bytes;
+  }
+  lbcu_spinor_s* sin[2] = {scratch_spinor(ctx, dr, LBCU_FULL, 300), scratch_spinor(ctx, dr, LBCU_FULL, 301)};
+  lbcu_spinor_s* sout[2] = {scratch_spinor(ctx, dr, LBCU_FULL, 302), scratch_spinor(ctx, dr, LBCU_FULL, 303)};
+  // the slots start free
+  for (int s = 0; s < 2; ++s) {
+    LBCU_CUDA(cudaEventRecord(P.ev_in_free[s], ctx->stream));
+    LBCU_CUDA(cudaEventRecord(P.ev_d2h[s], ctx->stream));
+  }
+  for (int k = 0; k < n; ++k) {
+    const int s = k & 1;
+    LBCU_CUDA(cudaStreamWaitEvent(P.h2d, P.ev_in_free[s], 0));
+    LBCU_CUDA(cudaMemcpyAsync(P.stage_in[s], in[k], bytes, cudaMemcpyHostToDevice, P.h2d));
+    LBCU_CUDA(cudaEventRecord(P.ev_h2d[s], P.h2d));
+    LBCU_CUDA(cudaStreamWaitEvent(ctx->stream, P.ev_h2d[s], 0));
+    launch_to_soa<double2>(ctx, static_cast<const double2*>(P.stage_in[s]), sin[s]->par[0], sin[s]->par[1], nv, 0);
+    LBCU_CUDA(cudaEventRecord(P.ev_in_free[s], ctx->stream));
+    HopCall hc;
+    hc.in = sin[s];
+    hc.out = sout[s];
+    hc.x = sin[s];
+    hc.g = g;
+    hc.out_parity = 2;
+    hc.a = 4.0 + mass;
+    hc.b = -0.5;
+    hop_apply(ctx, hc);
+    LBCU_CUDA(cudaStreamWaitEvent(ctx->stream, P.ev_d2h[s], 0));
+    launch_to_aos<double2>(ctx, sout[s]->par[0], sout[s]->par[1], static_cast<double2*>(P.stage_out[s]), nv);
+    LBCU_CUDA(cudaEventRecord(P.ev_out[s], ctx->stream));
+    LBCU_CUDA(cudaStreamWaitEvent(P.d2h, P.ev_out[s], 0));
+    LBCU_CUDA(cudaMemcpyAsync(out[k], P.stage_out[s], bytes, cudaMemcpyDeviceToHost, P.d2h));
+    LBCU_CUDA(cudaEventRecord(P.ev_d2h[s], P.d2h));
+  }
+  // the compute stream owns completion: later work and timing events see it
+  for (int s = 0; s < 2; ++s) LBCU_CUDA(cudaStreamWaitEvent(ctx->stream, P.ev_d2h[s], 0));
+  LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void host_pipe_release(lbcu_ctx_s* ctx) {
+  auto& P = ctx->pipe;
+  for (int s = 0; s < 2; ++s) {
+    if (P.stage_in[s]) cudaFree(P.stage_in[s]);
+    if (P.stage_out[s]) cudaFree(P.stage_out[s]);
+    if (P.ev_h2d[s]) cudaEventDestroy(P.ev_h2d[s]);
+    if (P.ev_in_free[s]) cudaEventDestroy(P.ev_in_free[s]);
+    if (P.ev_out[s]) cudaEventDestroy(P.ev_out[s]);
+    if (P.ev_d2h[s]) cudaEventDestroy(P.ev_d2h[s]);
+  }
+  if (P.h2d) cudaStreamDestroy(P.h2d);
+  if (P.d2h) cudaStreamDestroy(P.d2h);
+  P = lbcu_ctx_s::HostPipe{};
+}
+
 void spinor_download(lbcu_ctx_s* ctx, const lbcu_spinor_s* s, double* host) {
   const int nv = 4 * s->dr;
   const size_t bytes = static_cast<size_t>(ctx->geo.volume) * nv * sizeof(double2);
@@ -492,6 +571,15 @@ void dispatch_compact(const lbcu_gauge_s* g, int fmt, F&& f) {
   throw Error(LBCU_CONTRACT_VIOLATION, "no compact gauge format");
 }
 
+// formats that can only be expanded (they are uploaded in compact form)
+template <class F>
+void dispatch_expand(const lbcu_gauge_s* g, int fmt, F&& f) {
+  using std::integral_constant;
+  if (fmt == GF_AS4)
+    return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_AS4>{});
+  dispatch_compact(g, fmt, f);
+}
+
 int grid_for(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148 * 16)); }
 
 bool compaction_enabled(const lbcu_gauge_s* g) {
@@ -576,6 +664,31 @@ void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host) {
   LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// Links given as fundamental SU(N) elements; the representation is formed in
+// the kernels (GF_AS4: two-index antisymmetric of SU(4)).
+void gauge_upload_fundamental(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host) {
+  if (!(g->rep == LBCU_REP_ANTISYMMETRIC && g->n == 4))
+    throw Error(LBCU_CONFIG_ERROR,
+                "fundamental-link storage is implemented for the SU(4) antisymmetric representation");
+  const Geometry& geo = ctx->geo;
+  const int nv = 4 * 16;
+  const size_t bytes = static_cast<size_t>(geo.volume) * nv * sizeof(double2);
+  ensure_staging(ctx, bytes);
+  const size_t cbytes = 2 * static_cast<size_t>(nv) * geo.stride * sizeof(double2);
+  void* base = nullptr;
+  LBCU_CUDA(cudaMalloc(&base, cbytes));
+  LBCU_CUDA(cudaMemsetAsync(base, 0, cbytes, ctx->stream));
+  LBCU_CUDA(cudaMemcpyAsync(ctx->staging, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  double2* b = static_cast<double2*>(base);
+  launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b,
+                         b + static_cast<size_t>(nv) * geo.stride, nv, 0);
+  LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (g->base) LBCU_CUDA(cudaFree(g->base));
+  g->base = base;
+  g->fmt = GF_AS4;
+  g->compact_err = 0.0;
+}
+
 void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host) {
   const Geometry& geo = ctx->geo;
   const int nv = 4 * g->dr * g->dr;
@@ -587,7 +700,7 @@ void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host) {
   void* tmp = nullptr;
   if (g->fmt != GF_FULL) {
     LBCU_CUDA(cudaMalloc(&tmp, 2 * pstride * esz));
-    dispatch_compact(g, g->fmt, [&](auto Dc, auto Rc, auto Fc) {
+    dispatch_expand(g, g->fmt, [&](auto Dc, auto Rc, auto Fc) {
       constexpr int D = decltype(Dc)::value;
       constexpr bool REAL = decltype(Rc)::value;
       k_expand<D, REAL, decltype(Fc)::value><<<grid_for(8LL * geo.vh), 256, 0, ctx->stream>>>(

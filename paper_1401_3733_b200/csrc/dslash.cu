@@ -52,8 +52,27 @@ struct HopArgs {
   // antiperiodic time sign applied in-kernel (compact formats): the U_0 link
   // whose global time coordinate is bc_tlast carries a factor -1
   int bc_kernel, t_off, bc_tlast;
+  // L2-blocked schedule (sched_len > 0): the lattice is cut into spatial
+  // blocks of sched_bx x-planes (all y, z) and each block is swept along t;
+  // within one time slice a block is one contiguous cb range of sched_len
+  // sites, cut into sched_cpb chunks of blockDim.x. Both uses of every link
+  // and all 8 uses of every spinor then fall within ~2 slices of one block,
+  // a window sized to stay in L2 (hop_apply).
+  int sched_len, sched_cpb, sched_bx;
   Reduce red;
 };
+
+// block index (per parity) + thread -> cb site under the L2-blocked schedule
+__device__ __forceinline__ int sched_site(const HopArgs& A, int blk, bool& ok) {
+  const int Lt = A.g.L[0], Lx = A.g.L[1];
+  const int per_sb = Lt * A.sched_cpb;
+  const int sb = blk / per_sb, rem = blk - sb * per_sb;
+  const int t = rem / A.sched_cpb, chunk = rem - t * A.sched_cpb;
+  const int off = chunk * blockDim.x + threadIdx.x;
+  ok = off < A.sched_len;
+  const int row_sites = A.g.vh / (Lt * Lx);  // cb sites per x-plane of a slice
+  return (t * Lx + sb * A.sched_bx) * row_sites + off;
+}
 
 template <int D, int R0, int R1, int Q0, int Q1>
 __device__ __forceinline__ void reconstruct(double2 (&acc)[4][D], const double2 (&g)[2][D]) {
@@ -105,7 +124,7 @@ __device__ __forceinline__ const ElemT<D, REAL, FMT>* link_ptr(const void* gauge
 template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
 __device__ __forceinline__ void link_hop(double2 (&acc)[4][D], const ElemT<D, REAL, FMT>* p,
                                          long long st, const double2 (&h)[2][D]) {
-  if constexpr (D <= 3) {
+  if constexpr (D <= 3 || FMT == GF_AS4) {
     link_mul_acc<D, REAL, FMT, DAG, R0, R1, Q0, Q1>(acc, p, st, h);
   } else {
     double2 g[2][D];
@@ -175,16 +194,24 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
 
 template <int D, bool REAL, int FMT, bool BND, int EPI, int MINB>
 __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ HopArgs A) {
-  int par, idx;
+  int par, blk;
   if (A.both) {
     par = blockIdx.x & 1;
-    idx = (blockIdx.x >> 1) * blockDim.x + threadIdx.x;
+    blk = blockIdx.x >> 1;
   } else {
     par = A.par0;
-    idx = blockIdx.x * blockDim.x + threadIdx.x;
+    blk = blockIdx.x;
+  }
+  int idx;
+  bool ok;
+  if (A.sched_len > 0) {
+    idx = sched_site(A, blk, ok);
+  } else {
+    idx = blk * blockDim.x + threadIdx.x;
+    ok = idx < A.nsites;
   }
   double nrm[1] = {0.0};
-  if (idx < A.nsites) {
+  if (ok) {
     const int i = A.list[par] ? A.list[par][idx] : idx;
     int c[4], s;
     cb_coords(A.g, i, par, c, s);
@@ -334,9 +361,10 @@ void launch_hop_minb(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream
 }
 
 template <int D, bool REAL, int FMT>
-void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaStream_t s) {
+void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaStream_t s,
+                int blocks_override = 0) {
   if (nsites <= 0) return;
-  const int blocks = hop_blocks(nsites, npar, D);
+  const int blocks = blocks_override > 0 ? blocks_override : hop_blocks(nsites, npar, D);
   if constexpr (D <= 3) {
     if (env_int("LBCU_HOP_MINB", default_minb<D, REAL, FMT>()) == 3) {
       launch_hop_minb<D, REAL, FMT, 3>(A, bnd, epi, blocks, s);
@@ -361,7 +389,9 @@ void dispatch(int dr, bool real, int fmt, F&& f) {
         if (fmt == GF_R12) return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_R12>{});
         return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
       case 4: return f(integral_constant<int, 4>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
-      case 6: return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
+      case 6:
+        if (fmt == GF_AS4) return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_AS4>{});
+        return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
       case 10: return f(integral_constant<int, 10>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
     }
   } else {
@@ -436,13 +466,30 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     A.nsites = static_cast<int>(geo.vh);
     A.both = npar == 2;
     A.par0 = pars[0];
-    const int blocks = hop_blocks(A.nsites, npar, dr);
+    int blocks = hop_blocks(A.nsites, npar, dr);
+    // L2-blocked schedule: spatial blocks of bx x-planes whose two-slice
+    // working set (spinor in/out + links as stored) fits the L2 budget
+    if (env_int("LBCU_HOP_SCHED", 1)) {
+      const int lb = fmt == GF_SU2 ? 32 : fmt == GF_R12 ? 96 : fmt == GF_AS4 ? 256 : dr * dr * (real ? 8 : 16);
+      const double site_bytes = 128.0 * dr + (npar == 2 ? 4 : 8) * lb;
+      const double plane_bytes = site_bytes * geo.local[2] * geo.local[3];
+      const double budget = env_int("LBCU_HOP_L2MB", 32) * 1e6;
+      int bx = 1;
+      for (int d = 1; d <= geo.local[1]; ++d)
+        if (geo.local[1] % d == 0 && d * plane_bytes <= budget) bx = d;
+      if (bx < geo.local[1]) {  // a whole slice fits: the linear order is the same sweep
+        A.sched_bx = bx;
+        A.sched_len = bx * geo.local[2] * geo.local[3] / 2;
+        A.sched_cpb = (A.sched_len + kBlock - 1) / kBlock;
+        blocks = (geo.local[1] / bx) * geo.local[0] * A.sched_cpb * npar;
+      }
+    }
     if (reduce) {
       if (blocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
       A.red = Reduce{ctx->partials, ctx->ticket, c.result, 0, blocks};
     }
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s);
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s, blocks);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaGetLastError());

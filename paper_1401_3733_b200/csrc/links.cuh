@@ -28,7 +28,11 @@
 
 namespace lbcu {
 
-enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2 };
+//   GF_AS4  : two-index antisymmetric rep of SU(4) (dr = 6) stored as the
+//             fundamental 4 x 4 element (16 complex instead of 36); entries
+//             R_(ij),(kl) = u_ik u_jl - u_il u_jk (group.cpp:146-158) are
+//             formed in registers. Uploaded through lbcu_gauge_upload_fundamental.
+enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2, GF_AS4 = 3 };
 
 template <bool REAL>
 using LinkT = std::conditional_t<REAL, double, double2>;
@@ -36,10 +40,15 @@ using LinkT = std::conditional_t<REAL, double, double2>;
 template <int D, bool REAL, int FMT>
 struct LinkFmt {
   static constexpr bool valid = FMT == GF_FULL || (FMT == GF_SU2 && ((D == 2 && !REAL) || (D == 3 && REAL))) ||
-                                (FMT == GF_R12 && D == 3 && !REAL);
-  static constexpr int entries = FMT == GF_FULL ? D * D : (FMT == GF_SU2 ? 2 : 6);
+                                (FMT == GF_R12 && D == 3 && !REAL) || (FMT == GF_AS4 && D == 6 && !REAL);
+  static constexpr int entries =
+      FMT == GF_FULL ? D * D : (FMT == GF_SU2 ? 2 : (FMT == GF_R12 ? 6 : 16));
   using Elem = std::conditional_t<FMT == GF_FULL, LinkT<REAL>, double2>;
 };
+
+// lexicographic pairs i < j of SU(4) indices (group.cpp:119-124)
+__host__ __device__ constexpr int as4_i(int p) { return p < 3 ? 0 : (p < 5 ? 1 : 2); }
+__host__ __device__ constexpr int as4_j(int p) { return p < 3 ? p + 1 : (p < 5 ? p - 1 : 3); }
 
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -72,12 +81,20 @@ __device__ __forceinline__ void build_link(LinkT<REAL> (&u)[D * D],
     u[6] = fma(t3, a1, w * a2);
     u[7] = fma(t3, a2, -w * a1);
     u[8] = fma(t3, a3, d);
-  } else {  // GF_R12
+  } else if constexpr (FMT == GF_R12) {
 #pragma unroll
     for (int e = 0; e < 6; ++e) u[e] = s[e];
     u[6] = cconj(csub(cmul(u[1], u[5]), cmul(u[2], u[4])));
     u[7] = cconj(csub(cmul(u[2], u[3]), cmul(u[0], u[5])));
     u[8] = cconj(csub(cmul(u[0], u[4]), cmul(u[1], u[3])));
+  } else {  // GF_AS4: all 36 minors of the fundamental element
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int i = as4_i(p), j = as4_j(p), k = as4_i(q), l = as4_j(q);
+        u[p * 6 + q] = csub(cmul(s[i * 4 + k], s[j * 4 + l]), cmul(s[i * 4 + l], s[j * 4 + k]));
+      }
   }
 }
 
@@ -152,6 +169,35 @@ template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
 __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
                                              const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
                                              long long st, const double2 (&h)[2][D]) {
+  if constexpr (FMT == GF_AS4) {
+    // keep only the fundamental element in registers; form each minor when used
+    double2 s[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) s[e] = __ldg(p + (long long)e * st);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      double2 g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        // M_rc = R_rc, or conj(R_cr) for the dagger
+        const int pr = DAG ? c : r, pc = DAG ? r : c;
+        const int i = as4_i(pr), j = as4_j(pr), k = as4_i(pc), l = as4_j(pc);
+        const double2 e = csub(cmul(s[i * 4 + k], s[j * 4 + l]), cmul(s[i * 4 + l], s[j * 4 + k]));
+        if constexpr (DAG) {
+          cmac_conj(g0, e, h[0][c]);
+          cmac_conj(g1, e, h[1][c]);
+        } else {
+          cmac(g0, e, h[0][c]);
+          cmac(g1, e, h[1][c]);
+        }
+      }
+      acc[0][r] = cadd(acc[0][r], g0);
+      acc[1][r] = cadd(acc[1][r], g1);
+      acc[2][r] = cadd(acc[2][r], phm<Q0>(R0 == 0 ? g0 : g1));
+      acc[3][r] = cadd(acc[3][r], phm<Q1>(R1 == 0 ? g0 : g1));
+    }
+    return;
+  }
   [[maybe_unused]] LinkT<REAL> u[FMT == GF_FULL ? 1 : D * D];
   if constexpr (FMT != GF_FULL) load_link<D, REAL, FMT>(u, p, st);
 #pragma unroll

@@ -83,6 +83,14 @@ struct lbcu_ctx_s {
   void* staging = nullptr;  // device staging buffer for host<->device layout transposes
   size_t staging_bytes = 0;
   long long launches = 0;
+  // host-field pipeline (lbcu_dphi_host): 2 slots, copy-in / copy-out streams
+  struct HostPipe {
+    size_t bytes = 0;
+    void* stage_in[2] = {};
+    void* stage_out[2] = {};
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_in_free[2] = {}, ev_out[2] = {}, ev_d2h[2] = {};
+  } pipe;
 };
 
 namespace lbcu {
@@ -125,6 +133,11 @@ void spinor_upload(lbcu_ctx_s* ctx, lbcu_spinor_s* s, const double* host);
 void spinor_download(lbcu_ctx_s* ctx, const lbcu_spinor_s* s, double* host);
 void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host);
 void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host);
+void gauge_upload_fundamental(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host);
+// out[k] = D in[k] for host fields, transfers overlapped with the kernels
+void dphi_host_batch(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double mass, int n,
+                     const double* const* in, double* const* out);
+void host_pipe_release(lbcu_ctx_s* ctx);
 
 // helpers in api.cpp
 lbcu_spinor_s* scratch_spinor(lbcu_ctx_s* ctx, int dr, int subset, int slot);
