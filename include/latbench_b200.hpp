@@ -321,8 +321,8 @@ inline CgOutcome cg_solve_h(const GaugeField& g, double m, const SpinorField& rh
   lbcu_cg_settings s{st.tolerance, st.max_iterations};
   lbcu_cg_outcome o{};
   std::vector<double> hist(static_cast<size_t>(st.max_iterations));
-  check(lbcu_cg_solve_h(g.handle(), m, rhs.handle(), x.handle(), &s, &o, hist.data()),
-        o.iterations, o.best_residual);
+  const int rc = lbcu_cg_solve_h(g.handle(), m, rhs.handle(), x.handle(), &s, &o, hist.data());
+  check(rc, o.iterations, o.best_residual);  // o is filled before the status is raised
   return finish_outcome(std::move(x), o, std::move(hist));
 }
 
@@ -333,8 +333,8 @@ inline CgOutcome cg_solve_eo(const GaugeField& g, double m, const SpinorField& r
   lbcu_cg_settings s{st.tolerance, st.max_iterations};
   lbcu_cg_outcome o{};
   std::vector<double> hist(static_cast<size_t>(st.max_iterations));
-  check(lbcu_cg_solve_eo(g.handle(), m, rhs_even.handle(), x.handle(), &s, &o, hist.data()),
-        o.iterations, o.best_residual);
+  const int rc = lbcu_cg_solve_eo(g.handle(), m, rhs_even.handle(), x.handle(), &s, &o, hist.data());
+  check(rc, o.iterations, o.best_residual);
   return finish_outcome(std::move(x), o, std::move(hist));
 }
 
@@ -363,9 +363,9 @@ inline CgOutcome cg_solve(const LinearOp& op, const SpinorField& rhs, const CgSe
       return LBCU_CONTRACT_VIOLATION;
     }
   };
-  check(lbcu_cg_solve(rhs.worker().handle(), tramp, &box, rhs.handle(), x.handle(), &s, &o,
-                      hist.data()),
-        o.iterations, o.best_residual);
+  const int rc = lbcu_cg_solve(rhs.worker().handle(), tramp, &box, rhs.handle(), x.handle(), &s, &o,
+                               hist.data());
+  check(rc, o.iterations, o.best_residual);
   return finish_outcome(std::move(x), o, std::move(hist));
 }
 

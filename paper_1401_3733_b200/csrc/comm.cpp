@@ -169,6 +169,7 @@ struct NcclTransport final : Transport {
   int nranks() const override { return n_; }
   bool capturable() const override { return true; }
   void allreduce(int, double* dev, int n, cudaStream_t s) override {
+    if (n_ == 1) return;  // a sum over one rank is the identity (keeps graphs NCCL-free)
     nccl_check(NcclApi::get().AllReduce(dev, dev, n, ncclDouble, ncclSum, comm_, s),
                "ncclAllReduce");
   }
