@@ -156,6 +156,14 @@ int lbcu_gauge_set_compact(lbcu_gauge g, int enable);
  * kernels. Supported for the SU(4) antisymmetric representation (BASELINE
  * config 5): 16 instead of 36 complex numbers per link. */
 int lbcu_gauge_upload_fundamental(lbcu_gauge g, const double* host_fundamental);
+/* init_gauge_random on the device: the keyed generators of
+ * fields.cpp:86-107 / group.cpp:82-114 evaluated per link on the GPU
+ * (fundamental SU(2..4), the SU(2) adjoint, SU(4) antisymmetric via AS4
+ * storage; links = UNIT / HAAR / NEAR_UNIT). Agrees with the host generator
+ * to a few ulp (device transcendentals). */
+int lbcu_gauge_generate(lbcu_gauge g, int links, uint64_t seed, double eps);
+/* init_spinor_random (fields.cpp:22-40) on the device */
+int lbcu_spinor_random(lbcu_spinor s, uint64_t seed, uint64_t field_index);
 int lbcu_gauge_storage(lbcu_gauge g, int* format, double* reconstruction_error);
 int lbcu_gauge_destroy(lbcu_gauge g);
 

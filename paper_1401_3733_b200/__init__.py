@@ -145,6 +145,8 @@ def lib():
             "lbcu_gauge_destroy": (C.c_int, [_vp]),
             "lbcu_gauge_set_compact": (C.c_int, [_vp, C.c_int]),
             "lbcu_gauge_upload_fundamental": (C.c_int, [_vp, _dp]),
+            "lbcu_gauge_generate": (C.c_int, [_vp, C.c_int, C.c_uint64, C.c_double]),
+            "lbcu_spinor_random": (C.c_int, [_vp, C.c_uint64, C.c_uint64]),
             "lbcu_gauge_storage": (C.c_int, [_vp, _ip, _dp]),
             "lbcu_spinor_create": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
             "lbcu_spinor_upload": (C.c_int, [_vp, _dp]),
@@ -388,6 +390,11 @@ class GaugeField:
         _check(lib().lbcu_gauge_upload_fundamental(self._h, a.ctypes.data_as(_dp)))
         return self
 
+    def generate(self, seed: int, links=LINKS_HAAR, eps: float = 0.3):
+        """init_gauge_random on the device (keyed per global site, any decomposition)."""
+        _check(lib().lbcu_gauge_generate(self._h, int(links), int(seed), float(eps)))
+        return self
+
     def set_compact(self, enable: bool):
         """Allow (default) or forbid compact link storage for later uploads."""
         _check(lib().lbcu_gauge_set_compact(self._h, int(bool(enable))))
@@ -429,6 +436,11 @@ class SpinorField:
         if a.size != int(np.prod(self.host_shape)):
             raise ContractViolation(f"spinor upload expects {self.host_shape}, got {a.shape}")
         _check(lib().lbcu_spinor_upload(self._h, a.ctypes.data_as(_dp)))
+        return self
+
+    def randomize(self, seed: int, field_index: int):
+        """init_spinor_random on the device (fields.cpp:22-40)."""
+        _check(lib().lbcu_spinor_random(self._h, int(seed), int(field_index)))
         return self
 
     def upload_ptr(self, ptr: int):

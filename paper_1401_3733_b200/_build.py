@@ -45,6 +45,8 @@ def _compile(src, verbose):
         return obj
     # .cpp sources see the device headers (objects.hpp -> device.cuh): compile as CUDA
     cmd = [NVCC, *ARCH, *COMMON, "-x", "cu", "-c", src, "-o", obj]
+    if os.path.basename(src) == "generate.cu":
+        cmd += ["--fmad=false"]  # keep the host generators' rounding order
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -430,6 +430,34 @@ int lbcu_gauge_download(lbcu_gauge g, double* host) {
   API_END
 }
 
+int lbcu_gauge_generate(lbcu_gauge g, int links, uint64_t seed, double eps) {
+  API_BEGIN
+  need(g != nullptr, "lbcu_gauge_generate: null gauge");
+  if (links < LBCU_LINKS_UNIT || links > LBCU_LINKS_NEAR_UNIT)
+    throw Error(LBCU_CONFIG_ERROR, "unknown link generator");
+  lbcu_ctx_s* c = g->ctx;
+  bind(c);
+  if (g->rep == LBCU_REP_ANTISYMMETRIC && g->n == 4 && g->compact_ok) {
+    // fundamental elements are the AS4 storage itself
+    void* fund = gauge_generate_dense(c, g, links, seed, eps, true);
+    if (g->base) LBCU_CUDA(cudaFree(g->base));
+    g->base = fund;
+    g->fmt = 3;  // GF_AS4
+    g->compact_err = 0.0;
+  } else {
+    gauge_adopt_dense(c, g, gauge_generate_dense(c, g, links, seed, eps, false));
+  }
+  API_END
+}
+
+int lbcu_spinor_random(lbcu_spinor s, uint64_t seed, uint64_t field_index) {
+  API_BEGIN
+  need(s != nullptr, "lbcu_spinor_random: null field");
+  bind(s->ctx);
+  spinor_generate(s->ctx, s, seed, field_index);
+  API_END
+}
+
 int lbcu_gauge_upload_fundamental(lbcu_gauge g, const double* host) {
   API_BEGIN
   need(g && host, "lbcu_gauge_upload_fundamental: null argument");

@@ -613,6 +613,14 @@ void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host) {
     double2* b = static_cast<double2*>(full);
     launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b, b + pstride, nv, 0);
   }
+  gauge_adopt_dense(ctx, g, full);
+}
+
+// Take ownership of dense device links [2][4][dr*dr][stride] (no BC sign):
+// compress them when they reconstruct exactly, else bake the BC sign in.
+void gauge_adopt_dense(lbcu_ctx_s* ctx, lbcu_gauge_s* g, void* full) {
+  const Geometry& geo = ctx->geo;
+  const int dd = g->dr * g->dr;
   auto adopt = [&](void* base, int fmt) {
     if (g->base && g->base != base) LBCU_CUDA(cudaFree(g->base));
     g->base = base;

@@ -192,6 +192,9 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
   }
 }
 
+template <int D, bool REAL, int FMT, bool BND, int EPI>
+__device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1]);
+
 template <int D, bool REAL, int FMT, bool BND, int EPI, int MINB>
 __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ HopArgs A) {
   int par, blk;
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ 
     par = A.par0;
     blk = blockIdx.x;
   }
+  double nrm[1] = {0.0};
   int idx;
   bool ok;
   if (A.sched_len > 0) {
@@ -210,8 +214,13 @@ __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ 
     idx = blk * blockDim.x + threadIdx.x;
     ok = idx < A.nsites;
   }
-  double nrm[1] = {0.0};
-  if (ok) {
+  if (ok) site_body<D, REAL, FMT, BND, EPI>(A, par, idx, nrm);
+  if constexpr (EPI != EPI_STORE) block_reduce_finalize<1>(A.red, nrm);
+}
+
+template <int D, bool REAL, int FMT, bool BND, int EPI>
+__device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1]) {
+  {
     const int i = A.list[par] ? A.list[par][idx] : idx;
     int c[4], s;
     cb_coords(A.g, i, par, c, s);
@@ -256,7 +265,6 @@ __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ 
         }
       }
   }
-  if constexpr (EPI != EPI_STORE) block_reduce_finalize<1>(A.red, nrm);
 }
 
 // Pack one face of the input field into half-spinor records (see header).

@@ -134,6 +134,11 @@ void spinor_download(lbcu_ctx_s* ctx, const lbcu_spinor_s* s, double* host);
 void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host);
 void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host);
 void gauge_upload_fundamental(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host);
+void gauge_adopt_dense(lbcu_ctx_s* ctx, lbcu_gauge_s* g, void* full);
+// on-device keyed generation (generate.cu)
+void spinor_generate(lbcu_ctx_s* ctx, lbcu_spinor_s* s, uint64_t seed, uint64_t field);
+void* gauge_generate_dense(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, int links, uint64_t seed,
+                           double eps, bool fundamental);
 // out[k] = D in[k] for host fields, transfers overlapped with the kernels
 void dphi_host_batch(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double mass, int n,
                      const double* const* in, double* const* out);

@@ -24,7 +24,8 @@ def test_single_rank_nccl_world_runs_dphi_and_cg():
     lb.apply_dirac(b, gauge, a, 0.1)
     assert rel_l2(b.download(), O.port_dirac(L, 1, 0.1, g, s)) < 1e-12
     o = lb.cg_solve_eo(gauge, 0.1, lb.SpinorField(ctx, 3, lb.EVEN).upload(s), lb.CgSettings(1e-10, 500))
-    assert o.iterations == 23 and o.true_rel_residual < 2e-10
+    ref = O.port_cg(L, 1, 1, 0.1, g, s, 1e-10)
+    assert abs(o.iterations - ref["iterations"]) <= 1 and o.true_rel_residual < 2e-10
     ctx.barrier()
 
 
