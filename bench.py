@@ -224,18 +224,17 @@ def run_gpu(args, cfg):
     real = lb.rep_is_real(rep)
     links = {"haar": lb.LINKS_HAAR, "near_unit": lb.LINKS_NEAR_UNIT}[cfg["links"]]
     ctx = lb.Context(L, grid, rank, local if ws > 1 else 0, world)
-    g = lb.init_gauge_random(L, n, rep, 1, grid=grid, rank=rank, links=links, eps=0.3)
     s = lb.init_spinor_random(L, dr, 1, 0, grid=grid, rank=rank)
+    # links: the reference's keyed generator evaluated on the device (seed 1,
+    # keyed by global site: identical for any decomposition). SU(4) AS links
+    # are kept as their fundamental elements and represented in-kernel.
     gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T)
     if args.dense_links:
         gauge.set_compact(False)
-        gauge.upload(g)
-    elif rep == lb.ANTISYMMETRIC and n == 4:
-        # same keyed SU(4) elements before represent(): AS links formed in-kernel
-        gauge.upload_fundamental(lb.init_gauge_random(L, n, lb.FUNDAMENTAL, 1, grid=grid, rank=rank))
+    if args.host_links:
+        gauge.upload(lb.init_gauge_random(L, n, rep, 1, grid=grid, rank=rank, links=links, eps=0.3))
     else:
-        gauge.upload(g)
-    del g
+        gauge.generate(1, links=links, eps=0.3)
     fmt, fmt_err = gauge.storage()
     a = lb.SpinorField(ctx, dr).upload(s)
     b = lb.SpinorField(ctx, dr)
@@ -396,6 +395,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dense-links", action="store_true", help="store links as dense matrices")
+    ap.add_argument("--host-links", action="store_true", help="generate links on the host and upload")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]

@@ -258,6 +258,7 @@ int lbcu_ctx_create(lbcu_world w, int rank, int device, const int global[4], con
   dg.stride = g.stride;
 
   LBCU_CUDA(cudaSetDevice(device));
+  w->t->bind_device(device);
   LBCU_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   LBCU_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
   LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));

@@ -155,11 +155,16 @@ void nccl_check(ncclResult_t r, const char* what) {
 }
 
 struct NcclTransport final : Transport {
-  NcclTransport(int n, int rank, const unsigned char id[128]) : n_(n) {
-    auto& api = NcclApi::get();
-    ncclUniqueId uid;
-    std::memcpy(&uid, id, sizeof(uid));
-    nccl_check(api.CommInitRank(&comm_, n, uid, rank), "ncclCommInitRank");
+  // The communicator is created on first use by a context, after that
+  // context has made its device current (ncclCommInitRank binds the device).
+  NcclTransport(int n, int rank, const unsigned char id[128]) : n_(n), rank_(rank) {
+    NcclApi::get();  // fail early if libnccl is missing
+    std::memcpy(&uid_, id, sizeof(uid_));
+  }
+  void bind_device(int device) override {
+    if (comm_) return;
+    LBCU_CUDA(cudaSetDevice(device));
+    nccl_check(NcclApi::get().CommInitRank(&comm_, n_, uid_, rank_), "ncclCommInitRank");
     LBCU_CUDA(cudaMalloc(&scratch_, sizeof(double)));
   }
   ~NcclTransport() override {
@@ -168,17 +173,21 @@ struct NcclTransport final : Transport {
   }
   int nranks() const override { return n_; }
   bool capturable() const override { return true; }
+  ncclComm_t comm() const {
+    if (!comm_) throw Error(LBCU_TRANSPORT_ERROR, "NCCL world used before a context bound its device");
+    return comm_;
+  }
   void allreduce(int, double* dev, int n, cudaStream_t s) override {
     if (n_ == 1) return;  // a sum over one rank is the identity (keeps graphs NCCL-free)
-    nccl_check(NcclApi::get().AllReduce(dev, dev, n, ncclDouble, ncclSum, comm_, s),
+    nccl_check(NcclApi::get().AllReduce(dev, dev, n, ncclDouble, ncclSum, comm(), s),
                "ncclAllReduce");
   }
   void exchange(int, const std::vector<Msg>& msgs, cudaStream_t s) override {
     auto& api = NcclApi::get();
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (const auto& m : msgs) {
-      nccl_check(api.Send(m.send, m.bytes, ncclChar, m.peer_send, comm_, s), "ncclSend");
-      nccl_check(api.Recv(m.recv, m.bytes, ncclChar, m.peer_recv, comm_, s), "ncclRecv");
+      nccl_check(api.Send(m.send, m.bytes, ncclChar, m.peer_send, comm(), s), "ncclSend");
+      nccl_check(api.Recv(m.recv, m.bytes, ncclChar, m.peer_recv, comm(), s), "ncclRecv");
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
   }
@@ -191,7 +200,8 @@ struct NcclTransport final : Transport {
   }
 
  private:
-  int n_;
+  int n_, rank_;
+  ncclUniqueId uid_;
   ncclComm_t comm_ = nullptr;
   double* scratch_ = nullptr;
 };

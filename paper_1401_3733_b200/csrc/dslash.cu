@@ -194,6 +194,9 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
 
 template <int D, bool REAL, int FMT, bool BND, int EPI>
 __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1]);
+template <int D, int EPI>
+__device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const double2 (&acc)[4][D],
+                                         double (&nrm)[1]);
 
 template <int D, bool REAL, int FMT, bool BND, int EPI, int MINB>
 __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ HopArgs A) {
@@ -236,35 +239,52 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
     hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
     hop_mu<D, REAL, FMT, BND, 3>(acc, A, in, par, i, s, c);
 
-    const double2* x = A.x[par];
-    double2* out = A.out[par];
-    double2* r = A.r[par];
-    const double alpha = (EPI == EPI_CG) ? *A.alpha : 0.0;
-#pragma unroll
-    for (int sp = 0; sp < 4; ++sp)
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) {
-        const long long o = (long long)(sp * D + cc) * st + i;
-        const double bs = sp < 2 ? A.b : A.b * A.s5acc;
-        double2 v = cscale(bs, acc[sp][cc]);
-        if (x) {
-          const double as = sp < 2 ? A.a : A.a * A.s5x;
-          const double2 xv = ldg(x + o);
-          v.x = fma(as, xv.x, v.x);
-          v.y = fma(as, xv.y, v.y);
-        }
-        if constexpr (EPI == EPI_CG) {
-          double2 rv = r[o];
-          rv.x = fma(-alpha, v.x, rv.x);
-          rv.y = fma(-alpha, v.y, rv.y);
-          r[o] = rv;
-          nrm[0] = fma(rv.x, rv.x, fma(rv.y, rv.y, nrm[0]));
-        } else {
-          out[o] = v;
-          if constexpr (EPI == EPI_STORE_NORM) nrm[0] = fma(v.x, v.x, fma(v.y, v.y, nrm[0]));
-        }
-      }
+    epilogue<D, EPI>(A, par, i, acc, nrm);
   }
+}
+
+// out = a x + b acc (gamma5 signs folded), then store / store + |out|^2 /
+// CG residual update. Two phases: every load (x, r) is issued before any
+// store, and the pointers are restrict-qualified, so the 4 dr round trips
+// overlap instead of serialising behind possible aliasing.
+template <int D, int EPI>
+__device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const double2 (&acc)[4][D],
+                                         double (&nrm)[1]) {
+  const long long st = A.g.stride;
+  const double2* __restrict__ x = A.x[par];
+  double2* __restrict__ out = A.out[par];
+  double2* __restrict__ r = A.r[par];
+  double2 xv[4][D], rv[4][D];
+#pragma unroll
+  for (int sp = 0; sp < 4; ++sp)
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) {
+      const long long o = (long long)(sp * D + cc) * st + i;
+      xv[sp][cc] = x ? ldg(x + o) : make_double2(0.0, 0.0);
+      if constexpr (EPI == EPI_CG) rv[sp][cc] = __ldcg(r + o);
+    }
+  const double alpha = (EPI == EPI_CG) ? *A.alpha : 0.0;
+#pragma unroll
+  for (int sp = 0; sp < 4; ++sp)
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) {
+      const long long o = (long long)(sp * D + cc) * st + i;
+      const double bs = sp < 2 ? A.b : A.b * A.s5acc;
+      const double as = sp < 2 ? A.a : A.a * A.s5x;
+      double2 v = cscale(bs, acc[sp][cc]);
+      v.x = fma(as, xv[sp][cc].x, v.x);
+      v.y = fma(as, xv[sp][cc].y, v.y);
+      if constexpr (EPI == EPI_CG) {
+        double2 w = rv[sp][cc];
+        w.x = fma(-alpha, v.x, w.x);
+        w.y = fma(-alpha, v.y, w.y);
+        r[o] = w;
+        nrm[0] = fma(w.x, w.x, fma(w.y, w.y, nrm[0]));
+      } else {
+        out[o] = v;
+        if constexpr (EPI == EPI_STORE_NORM) nrm[0] = fma(v.x, v.x, fma(v.y, v.y, nrm[0]));
+      }
+    }
 }
 
 // Pack one face of the input field into half-spinor records (see header).

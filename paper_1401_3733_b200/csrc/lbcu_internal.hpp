@@ -84,6 +84,8 @@ struct Transport {
   };
   virtual void exchange(int rank, const std::vector<Msg>& msgs, cudaStream_t s) = 0;
   virtual void barrier(int rank) = 0;
+  // called by each context after it selected its device
+  virtual void bind_device(int /*device*/) {}
 };
 
 std::unique_ptr<Transport> make_single_transport();
