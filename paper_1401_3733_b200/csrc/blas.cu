@@ -143,23 +143,7 @@ __global__ void k_cg_alpha(CgState* st, const double* pap) {
 // convergence, beta, rr <- rr_new; optionally drives a graph while-loop.
 __global__ void k_cg_end(CgState* st, const double* rr_new, double* hist,
                          cudaGraphConditionalHandle handle, int use_graph) {
-  const double rrn = *rr_new;
-  const double rel = sqrt(rrn) / st->bnorm;
-  const long long k = st->k;
-  hist[k] = rel;
-  st->rel = rel;
-  st->rr_new = rrn;
-  if (rel < st->best) st->best = rel;
-  st->k = k + 1;
-  if (rel < st->tol) {
-    st->conv = 1;
-    st->done = 1;
-  } else if (k + 1 >= st->maxit) {
-    st->done = 1;
-  }
-  st->beta = rrn / st->rr;
-  st->rr = rrn;
-  if (use_graph) cudaGraphSetConditional(handle, st->done ? 0u : 1u);
+  cg_post_end(st, *rr_new, hist, static_cast<unsigned long long>(handle), use_graph);
 }
 
 // ---- layout transposes -----------------------------------------------------

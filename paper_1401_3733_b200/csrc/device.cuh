@@ -113,12 +113,55 @@ __device__ __forceinline__ T ldg(const T* p) {
 // partials to part[(offset + blockIdx) * NR + k]. The block that arrives last
 // on the ticket sums all partials in a fixed order and writes result[k], so
 // the value does not depend on block scheduling.
+// Device CG state (one per context, solver.cpp).
+struct CgState {
+  double rr, rr_new, pap, alpha, beta, bnorm, tol, best, rel;
+  long long k, maxit;
+  int conv, done;
+};
+
+// CG scalar steps (solver.cpp:53-69), run by one thread: either a 1-thread
+// kernel after a multi-rank allreduce, or fused into the last block of the
+// reduction that produced the value (single rank).
+__device__ __forceinline__ void cg_post_alpha(CgState* st, double pap) {
+  st->pap = pap;
+  st->alpha = st->rr / pap;
+}
+
+__device__ __forceinline__ void cg_post_end(CgState* st, double rrn, double* hist,
+                                            unsigned long long handle, int use_graph) {
+  const double rel = sqrt(rrn) / st->bnorm;
+  const long long k = st->k;
+  hist[k] = rel;
+  st->rel = rel;
+  st->rr_new = rrn;
+  if (rel < st->best) st->best = rel;
+  st->k = k + 1;
+  if (rel < st->tol) {
+    st->conv = 1;
+    st->done = 1;
+  } else if (k + 1 >= st->maxit) {
+    st->done = 1;
+  }
+  st->beta = rrn / st->rr;
+  st->rr = rrn;
+  if (use_graph) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(handle), st->done ? 0u : 1u);
+}
+
+enum RedPost { POST_NONE = 0, POST_ALPHA = 1, POST_END = 2 };
+
 struct Reduce {
   double* part;        // partials, >= total_blocks * NR
   unsigned* ticket;    // zero between reductions
   double* result;      // NR outputs
   int offset;          // this launch's first partial slot
   int total_blocks;    // partial slots over all launches that feed this result
+  // optional CG scalar step on result[0] by the finishing block
+  int post;
+  CgState* cg;
+  double* hist;
+  unsigned long long handle;
+  int use_graph;
 };
 
 template <int NR>
@@ -171,6 +214,8 @@ __device__ __forceinline__ void block_reduce_finalize(const Reduce& R, double (&
       R.result[k] = s;
     }
     *R.ticket = 0u;
+    if (R.post == POST_ALPHA) cg_post_alpha(R.cg, R.result[0]);
+    else if (R.post == POST_END) cg_post_end(R.cg, R.result[0], R.hist, R.handle, R.use_graph);
   }
 }
 

@@ -365,6 +365,7 @@ int default_minb() {
   // profiles/r01_tune_*: a cap of 3 blocks/SM helps D = 2 (13 % with SU(2)
   // links) and the real adjoint; dense/R12 SU(3) runs best uncapped on the eo
   // hop; larger D spill under any cap.
+  if (D == 2 && FMT == GF_SU2) return 4;  // r01_tune_minb_su2 (1 % over 3)
   if (D == 2 || (D == 3 && REAL)) return 3;
   if (D == 3 && FMT == GF_FULL) return 3;
   return 1;
@@ -394,7 +395,18 @@ void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaS
   if (nsites <= 0) return;
   const int blocks = blocks_override > 0 ? blocks_override : hop_blocks(nsites, npar, D);
   if constexpr (D <= 3) {
-    if (env_int("LBCU_HOP_MINB", default_minb<D, REAL, FMT>()) == 3) {
+    const int minb = env_int("LBCU_HOP_MINB", default_minb<D, REAL, FMT>());
+    if constexpr (D == 2 && FMT == GF_SU2) {
+      if (minb == 4) {
+        launch_hop_minb<D, REAL, FMT, 4>(A, bnd, epi, blocks, s);
+        return;
+      }
+      if (minb == 5) {
+        launch_hop_minb<D, REAL, FMT, 5>(A, bnd, epi, blocks, s);
+        return;
+      }
+    }
+    if (minb == 3) {
       launch_hop_minb<D, REAL, FMT, 3>(A, bnd, epi, blocks, s);
       return;
     }
@@ -514,7 +526,8 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     }
     if (reduce) {
       if (blocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
-      A.red = Reduce{ctx->partials, ctx->ticket, c.result, 0, blocks};
+      A.red = Reduce{ctx->partials, ctx->ticket, c.result, 0, blocks,
+                     c.post, ctx->dcg, ctx->dhist, c.handle, c.use_graph};
     }
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
       launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s, blocks);
@@ -535,6 +548,8 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   }
   if (reduce && total_blocks > ctx->max_partials)
     throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
+  if (c.post != POST_NONE)
+    throw Error(LBCU_CONTRACT_VIOLATION, "fused CG scalar steps need a single rank");
   // one exchange per output parity keeps the message buffers simple
   for (int k = 0; k < npar; ++k) {
     const int p = pars[k], q = p ^ 1;

@@ -38,13 +38,6 @@ namespace lbcu {
 
 enum Epi { EPI_STORE = 0, EPI_STORE_NORM = 1, EPI_CG = 2 };
 
-// Device CG state (one per context), see cg.cu.
-struct CgState {
-  double rr, rr_new, pap, alpha, beta, bnorm, tol, best, rel;
-  long long k, maxit;
-  int conv, done;
-};
-
 struct HaloBufs {
   double2* send[8] = {};
   double2* recv[8] = {};
@@ -108,6 +101,10 @@ struct HopCall {
   int epi = EPI_STORE;
   const double* alpha = nullptr;  // EPI_CG scalar (device)
   double* result = nullptr;       // reduction output (device), EPI != STORE
+  // CG scalar step fused into the reduction's last block (single rank only)
+  int post = POST_NONE;
+  unsigned long long handle = 0;
+  int use_graph = 0;
 };
 void hop_apply(lbcu_ctx_s* ctx, const HopCall& c);
 

@@ -57,6 +57,27 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
                 int use_graph) {
   Transport* T = ctx->world->t.get();
   const double A = 4.0 + F.mass;
+  // one rank: alpha and the end-of-iteration step run in the last block of
+  // the reductions that produce pAp and rr' (two launches fewer per iteration)
+  const bool fuse = T->nranks() == 1 && std::getenv("LBCU_CG_FUSE_SCALARS") == nullptr;
+  auto scalar_alpha = [&](HopCall& h) {
+    if (fuse) {
+      h.post = POST_ALPHA;
+      return;
+    }
+  };
+  auto scalar_end = [&](HopCall& h) {
+    if (fuse) {
+      h.post = POST_END;
+      h.handle = handle;
+      h.use_graph = use_graph;
+    }
+  };
+  auto after_pap = [&] {
+    if (fuse) return;
+    T->allreduce(ctx->rank, slot(ctx, kSlotPap), 1, ctx->stream);
+    cg_scalar_alpha(ctx, slot(ctx, kSlotPap));
+  };
   cg_p_update(ctx, p, r, x);
   if (F.kind == Fused::EO) {
     HopCall a;  // t_o = H_oe p_e
@@ -75,9 +96,9 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
     b.b = -1.0 / (4.0 * A);
     b.epi = EPI_STORE_NORM;
     b.result = slot(ctx, kSlotPap);
+    scalar_alpha(b);
     hop_apply(ctx, b);
-    T->allreduce(ctx->rank, slot(ctx, kSlotPap), 1, ctx->stream);
-    cg_scalar_alpha(ctx, slot(ctx, kSlotPap));
+    after_pap();
     HopCall c;  // t_o = H_oe g5 q
     c.in = q;
     c.out = t;
@@ -98,6 +119,7 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
     d.epi = EPI_CG;
     d.alpha = &ctx->dcg->alpha;
     d.result = slot(ctx, kSlotRR);
+    scalar_end(d);
     hop_apply(ctx, d);
   } else {
     HopCall a;  // q = D p ; |q|^2 = <p, D^dag D p>
@@ -110,9 +132,9 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
     a.b = -0.5;
     a.epi = EPI_STORE_NORM;
     a.result = slot(ctx, kSlotPap);
+    scalar_alpha(a);
     hop_apply(ctx, a);
-    T->allreduce(ctx->rank, slot(ctx, kSlotPap), 1, ctx->stream);
-    cg_scalar_alpha(ctx, slot(ctx, kSlotPap));
+    after_pap();
     HopCall b;  // Ap = g5 D g5 q ; r -= alpha Ap ; |r|^2
     b.in = q;
     b.out = q;  // unused by EPI_CG (in == out is never written)
@@ -127,8 +149,10 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
     b.epi = EPI_CG;
     b.alpha = &ctx->dcg->alpha;
     b.result = slot(ctx, kSlotRR);
+    scalar_end(b);
     hop_apply(ctx, b);
   }
+  if (fuse) return;
   T->allreduce(ctx->rank, slot(ctx, kSlotRR), 1, ctx->stream);
   cg_scalar_end(ctx, slot(ctx, kSlotRR), handle, use_graph);
 }

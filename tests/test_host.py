@@ -170,6 +170,21 @@ def test_face_schedule_pairs_halo_records(grid, qpar):
             off += count[f]
 
 
+def test_bench_decompose_rules():
+    """bench.py: T first while the local T stays >= 8 and even, then Z."""
+    import bench
+    assert bench.decompose([32, 32, 32, 32], 8) == [4, 1, 1, 2]
+    assert bench.decompose([96, 48, 48, 48], 8) == [8, 1, 1, 1]
+    assert bench.decompose([40, 40, 40, 40], 8) == [4, 1, 1, 2]
+    assert bench.decompose([64, 32, 32, 32], 8) == [8, 1, 1, 1]
+    assert bench.decompose([32, 32, 32, 32], 2) == [2, 1, 1, 1]
+    for L in ([32] * 4, [96, 48, 48, 48], [40] * 4, [64, 32, 32, 32]):
+        for n in (1, 2, 4, 8):
+            g = bench.decompose(L, n)
+            assert int(np.prod(g)) == n
+            assert lb.local_extents(L, g)  # valid even-odd decomposition
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
