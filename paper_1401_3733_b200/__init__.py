@@ -33,7 +33,7 @@ from typing import Callable, Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblbcu.so")
+LIB_PATH = os.environ.get("LBCU_LIBRARY") or os.path.join(_PKG, "liblbcu.so")
 
 FUNDAMENTAL, ADJOINT, SYMMETRIC, ANTISYMMETRIC = 0, 1, 2, 3
 SQNORM, MULADD, DIRAC = 0, 1, 2

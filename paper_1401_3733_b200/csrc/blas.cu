@@ -64,7 +64,7 @@ __global__ void k_xpay(double2* __restrict__ y, const double2* __restrict__ x, s
   }
 }
 
-// negate spin components 2,3 of every parity block: [2 dr stride, 4 dr stride)
+// negate spin components 2,3: the upper half [2 dr 32, 4 dr 32) of every tile
 __global__ void k_gamma5(double2* __restrict__ f, size_t block_elems, size_t half, int nblocks) {
   const size_t n = half * nblocks;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -151,10 +151,11 @@ __device__ __forceinline__ double neg(double a) { return -a; }
 __device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
 
 // Host order: site-major local lexicographic records of nv entries.
-// Device order: per parity block, entry-major [nv][stride] over cb sites.
+// Device order: per parity block, nv / ng groups (link: one per mu) of ng
+// elements per site, each group stride x ng elements in 32-site tiles (eidx).
 // A block stages TS consecutive sites (TS even -> TS/2 cb sites per parity).
 template <class T>
-__global__ void k_aos_to_soa(const T* __restrict__ src, T* dst0, T* dst1, int nv, long long vol,
+__global__ void k_aos_to_soa(const T* __restrict__ src, T* dst0, T* dst1, int nv, int ng, long long vol,
                              long long stride, int TS, DevGeo g, int sign_entries, int sign_t,
                              int t_off) {
   extern __shared__ unsigned char smraw[];
@@ -177,12 +178,12 @@ __global__ void k_aos_to_soa(const T* __restrict__ src, T* dst0, T* dst1, int nv
     cb_coords(g, (int)cb, p, c, s);
     T v = sm[(s - s0) * nv + k];
     if (k < sign_entries && c[0] + t_off == sign_t) v = neg(v);
-    dst[(long long)k * stride + cb] = v;
+    dst[(k / ng) * ng * stride + eidx(ng, k % ng, cb)] = v;
   }
 }
 
 template <class T>
-__global__ void k_soa_to_aos(const T* src0, const T* src1, T* __restrict__ dst, int nv,
+__global__ void k_soa_to_aos(const T* src0, const T* src1, T* __restrict__ dst, int nv, int ng,
                              long long vol, long long stride, int TS, DevGeo g) {
   extern __shared__ unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
@@ -195,7 +196,7 @@ __global__ void k_soa_to_aos(const T* src0, const T* src1, T* __restrict__ dst, 
     int c[4], s;
     cb_coords(g, (int)cb, p, c, s);
     const T* src = p ? src1 : src0;
-    sm[(s - s0) * nv + k] = src ? src[(long long)k * stride + cb] : T{};
+    sm[(s - s0) * nv + k] = src ? src[(k / ng) * ng * stride + eidx(ng, k % ng, cb)] : T{};
   }
   __syncthreads();
   const int tile = TS * nv;
@@ -260,7 +261,7 @@ void blas_zero(lbcu_ctx_s* ctx, lbcu_spinor_s* f) {
 }
 
 void blas_gamma5(lbcu_ctx_s* ctx, lbcu_spinor_s* f) {
-  const size_t blk = static_cast<size_t>(4 * f->dr) * ctx->geo.stride;
+  const size_t blk = static_cast<size_t>(4 * f->dr) * kTile;
   const int nblocks = static_cast<int>(f->elems / blk);
   const size_t half = blk / 2;
   k_gamma5<<<flat_blocks(ctx, half * nblocks), kThreads, 0, ctx->stream>>>(f->base, blk, half, nblocks);
@@ -307,26 +308,28 @@ void cg_scalar_end(lbcu_ctx_s* ctx, const double* rr_new, unsigned long long han
 }
 
 template <class T>
-static void launch_to_soa(lbcu_ctx_s* ctx, const T* src, T* d0, T* d1, int nv, int sign_entries) {
+static void launch_to_soa(lbcu_ctx_s* ctx, const T* src, T* d0, T* d1, int nv, int sign_entries,
+                          int ng = 0) {
   const Geometry& geo = ctx->geo;
   const int TS = tile_sites<T>(nv);
   const size_t smem = static_cast<size_t>(TS) * nv * sizeof(T);
   const int blocks = static_cast<int>((geo.volume + TS - 1) / TS);
   const int sign_t = sign_entries ? geo.global[0] - 1 : -1;
   const int t_off = geo.coords[0] * geo.local[0];
-  k_aos_to_soa<T><<<blocks, 256, smem, ctx->stream>>>(src, d0, d1, nv, geo.volume, geo.stride, TS,
+  k_aos_to_soa<T><<<blocks, 256, smem, ctx->stream>>>(src, d0, d1, nv, ng ? ng : nv, geo.volume, geo.stride, TS,
                                                       ctx->dgeo, sign_entries, sign_t, t_off);
   ctx->launches++;
   LBCU_CUDA(cudaGetLastError());
 }
 
 template <class T>
-static void launch_to_aos(lbcu_ctx_s* ctx, const T* s0, const T* s1, T* dst, int nv) {
+static void launch_to_aos(lbcu_ctx_s* ctx, const T* s0, const T* s1, T* dst, int nv, int ng = 0) {
   const Geometry& geo = ctx->geo;
   const int TS = tile_sites<T>(nv);
   const size_t smem = static_cast<size_t>(TS) * nv * sizeof(T);
   const int blocks = static_cast<int>((geo.volume + TS - 1) / TS);
-  k_soa_to_aos<T><<<blocks, 256, smem, ctx->stream>>>(s0, s1, dst, nv, geo.volume, geo.stride, TS, ctx->dgeo);
+  k_soa_to_aos<T><<<blocks, 256, smem, ctx->stream>>>(s0, s1, dst, nv, ng ? ng : nv, geo.volume, geo.stride, TS,
+                                                      ctx->dgeo);
   ctx->launches++;
   LBCU_CUDA(cudaGetLastError());
 }
@@ -457,11 +460,11 @@ __global__ void k_compress(const LinkT<REAL>* __restrict__ full, double2* __rest
   double worst = 0.0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
     const long long blk = t / vh, cb = t % vh;
-    const LinkT<REAL>* f = full + blk * D * D * stride + cb;
-    double2* cp = compact + blk * E * stride + cb;
+    const LinkT<REAL>* f = site_ptr<D * D>(full + blk * D * D * stride, cb);
+    double2* cp = site_ptr<E>(compact + blk * E * stride, cb);
     LinkT<REAL> u[D * D];
 #pragma unroll
-    for (int e = 0; e < D * D; ++e) u[e] = f[(long long)e * stride];
+    for (int e = 0; e < D * D; ++e) u[e] = f[(long long)e * kTile];
     double2 st[E];
     if constexpr (FMT == GF_SU2 && !REAL) {
       st[0] = u[0];
@@ -499,7 +502,7 @@ __global__ void k_compress(const LinkT<REAL>* __restrict__ full, double2* __rest
       for (int e = 0; e < 6; ++e) st[e] = u[e];
     }
 #pragma unroll
-    for (int e = 0; e < E; ++e) cp[(long long)e * stride] = st[e];
+    for (int e = 0; e < E; ++e) cp[(long long)e * kTile] = st[e];
     // validate: rebuild from the stored entries and compare with the dense link
     LinkT<REAL> r[D * D];
     build_link<D, REAL, FMT>(r, st);
@@ -523,9 +526,10 @@ __global__ void k_expand(const double2* __restrict__ compact, LinkT<REAL>* __res
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
     const long long blk = t / vh, cb = t % vh;
     LinkT<REAL> u[D * D];
-    load_link<D, REAL, FMT>(u, compact + blk * E * stride + cb, stride);
+    load_link<D, REAL, FMT>(u, site_ptr<E>(compact + blk * E * stride, cb), kTile);
+    LinkT<REAL>* f = site_ptr<D * D>(full + blk * D * D * stride, cb);
 #pragma unroll
-    for (int e = 0; e < D * D; ++e) full[blk * D * D * stride + (long long)e * stride + cb] = u[e];
+    for (int e = 0; e < D * D; ++e) f[(long long)e * kTile] = u[e];
   }
 }
 
@@ -538,8 +542,11 @@ __global__ void k_bake_sign(T* full, long long stride, int entries, DevGeo g, in
     int c[4], s;
     cb_coords(g, cb, par, c, s);
     if (c[0] + t_off != tlast) continue;
-    T* base = full + (long long)par * 4 * entries * stride + cb;  // mu = 0 block
-    for (int e = 0; e < entries; ++e) base[(long long)e * stride] = neg(base[(long long)e * stride]);
+    T* base = full + (long long)par * 4 * entries * stride;  // mu = 0 block
+    for (int e = 0; e < entries; ++e) {
+      const long long o = eidx(entries, e, cb);
+      base[o] = neg(base[o]);
+    }
   }
 }
 
@@ -592,10 +599,10 @@ void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host) {
   const size_t pstride = static_cast<size_t>(nv) * geo.stride;
   if (g->real) {
     double* b = static_cast<double*>(full);
-    launch_to_soa<double>(ctx, static_cast<const double*>(ctx->staging), b, b + pstride, nv, 0);
+    launch_to_soa<double>(ctx, static_cast<const double*>(ctx->staging), b, b + pstride, nv, 0, dd);
   } else {
     double2* b = static_cast<double2*>(full);
-    launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b, b + pstride, nv, 0);
+    launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b, b + pstride, nv, 0, dd);
   }
   gauge_adopt_dense(ctx, g, full);
 }
@@ -673,7 +680,7 @@ void gauge_upload_fundamental(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* ho
   LBCU_CUDA(cudaMemcpyAsync(ctx->staging, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
   double2* b = static_cast<double2*>(base);
   launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b,
-                         b + static_cast<size_t>(nv) * geo.stride, nv, 0);
+                         b + static_cast<size_t>(nv) * geo.stride, nv, 0, 16);
   LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
   if (g->base) LBCU_CUDA(cudaFree(g->base));
   g->base = base;
@@ -704,10 +711,10 @@ void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host) {
   }
   if (g->real) {
     const double* b = static_cast<const double*>(full);
-    launch_to_aos<double>(ctx, b, b + pstride, static_cast<double*>(ctx->staging), nv);
+    launch_to_aos<double>(ctx, b, b + pstride, static_cast<double*>(ctx->staging), nv, nv / 4);
   } else {
     const double2* b = static_cast<const double2*>(full);
-    launch_to_aos<double2>(ctx, b, b + pstride, static_cast<double2*>(ctx->staging), nv);
+    launch_to_aos<double2>(ctx, b, b + pstride, static_cast<double2*>(ctx->staging), nv, nv / 4);
   }
   LBCU_CUDA(cudaMemcpyAsync(host, ctx->staging, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   LBCU_CUDA(cudaStreamSynchronize(ctx->stream));

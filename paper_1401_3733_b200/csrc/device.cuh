@@ -8,6 +8,21 @@
 
 namespace lbcu {
 
+// Per-site arrays (spinor components, link entries) of one parity block are
+// tiled by 32 cb sites: element e of site i, with nc elements per site, sits at
+//   (i / 32) * nc * 32 + e * 32 + i % 32.
+// A warp over 32 consecutive sites still reads one 512-byte segment per
+// element, and element offsets inside a tile are compile-time immediates
+// (one 64-bit site address per neighbour instead of one per element).
+constexpr int kTile = 32;
+__host__ __device__ __forceinline__ long long eidx(int nc, int e, long long i) {
+  return (i >> 5) * (32LL * nc) + 32LL * e + (i & 31);
+}
+template <int NC, class T>
+__host__ __device__ __forceinline__ T* site_ptr(T* base, long long i) {
+  return base + (i >> 5) * (32LL * NC) + (i & 31);
+}
+
 // Local lattice as seen by a kernel. Sites of one parity are stored in
 // "checkerboard" order cb = s >> 1 of the local lexicographic index s
 // (t,x,y,z; z fastest). Every local extent is even, so (z, z+1) pairs split

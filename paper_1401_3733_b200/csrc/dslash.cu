@@ -1,4 +1,4 @@
-// Wilson hopping term on the even-odd SoA layout (sm_100a).
+// Wilson hopping term on the even-odd tiled layout (sm_100a).
 //
 // Replaces the reference's scalar site loop dirac_site/dirac_interior
 // (proj/include/latbench/kernel_ops.hpp:128-215) and, for decomposed runs,
@@ -13,10 +13,11 @@
 // optionally storing it, taking |out|^2 block partials, or instead applying
 // the CG residual update r -= alpha out and reducing |r|^2 (out never stored).
 //
-// Memory layout: every spinor component / link entry is a contiguous
-// double2 (or double for real links) array over checkerboard sites, so a warp
-// issues fully coalesced 512-byte (LDG.128) loads for each component. Links
-// are read in their storage format (links.cuh) and rebuilt in registers.
+// Memory layout: spinor components / link entries are tiled by 32
+// checkerboard sites (device.cuh: element e of site i at tile(i)*nc*32 +
+// e*32 + i%32), so a warp issues fully coalesced 512-byte (LDG.128) loads for
+// each component with compile-time element offsets. Links are read in their
+// storage format (links.cuh) and rebuilt in registers.
 //
 // Decomposed directions: boundary sites are handled by a second launch that
 // reads half-spinor halos produced by pack_kernel on the neighbour rank:
@@ -39,7 +40,7 @@ struct HopArgs {
   double2* out[2];       // output blocks by output parity
   const double2* x[2];   // diagonal-term blocks by output parity (nullable)
   double2* r[2];         // CG residual blocks by output parity
-  const void* gauge;     // [2 parity][4 mu][entries][stride] in the storage format
+  const void* gauge;     // [2 parity][4 mu] blocks of entries x stride (tiled), storage format
   double a, b, s5in, s5x, s5acc;
   const double* alpha;
   int par0;    // output parity of a single-parity launch
@@ -85,16 +86,22 @@ __device__ __forceinline__ void reconstruct(double2 (&acc)[4][D], const double2 
   }
 }
 
+// element stride inside a 32-site tile (device.cuh); the block stride `st`
+// only locates (parity, mu) blocks
+__device__ __forceinline__ long long estride(long long) { return kTile; }
+
 // h_a = psi_a + F_a * s5 * psi_{p_a}: spin projection of the spinor at cb site nb
 template <int D, int P0, int P1, int F0, int F1>
 __device__ __forceinline__ void project(double2 (&h)[2][D], const double2* __restrict__ in,
                                         long long st, int nb, double s5) {
+  const double2* __restrict__ q = site_ptr<4 * D>(in, nb);
+  const long long es = estride(st);
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    const double2 a0 = ldg(in + (long long)(0 * D + c) * st + nb);
-    const double2 a1 = ldg(in + (long long)(1 * D + c) * st + nb);
-    const double2 b0 = ldg(in + (long long)(P0 * D + c) * st + nb);
-    const double2 b1 = ldg(in + (long long)(P1 * D + c) * st + nb);
+    const double2 a0 = ldg(q + (long long)(0 * D + c) * es);
+    const double2 a1 = ldg(q + (long long)(1 * D + c) * es);
+    const double2 b0 = ldg(q + (long long)(P0 * D + c) * es);
+    const double2 b1 = ldg(q + (long long)(P1 * D + c) * es);
     h[0][c] = cadd(a0, phm<F0>(cscale(s5, b0)));
     h[1][c] = cadd(a1, phm<F1>(cscale(s5, b1)));
   }
@@ -116,7 +123,7 @@ template <int D, bool REAL, int FMT>
 __device__ __forceinline__ const ElemT<D, REAL, FMT>* link_ptr(const void* gauge, long long st,
                                                                int par, int mu, int site) {
   constexpr int E = LinkFmt<D, REAL, FMT>::entries;
-  return static_cast<const ElemT<D, REAL, FMT>*>(gauge) + (long long)(par * 4 + mu) * E * st + site;
+  return site_ptr<E>(static_cast<const ElemT<D, REAL, FMT>*>(gauge) + (long long)(par * 4 + mu) * E * st, site);
 }
 
 // Multiply by the link and reconstruct into acc. Small dr: row-fused (no
@@ -125,10 +132,10 @@ template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
 __device__ __forceinline__ void link_hop(double2 (&acc)[4][D], const ElemT<D, REAL, FMT>* p,
                                          long long st, const double2 (&h)[2][D]) {
   if constexpr (D <= 3 || FMT == GF_AS4) {
-    link_mul_acc<D, REAL, FMT, DAG, R0, R1, Q0, Q1>(acc, p, st, h);
+    link_mul_acc<D, REAL, FMT, DAG, R0, R1, Q0, Q1>(acc, p, estride(st), h);
   } else {
     double2 g[2][D];
-    link_mul<D, REAL, FMT, DAG>(g, p, st, h);
+    link_mul<D, REAL, FMT, DAG>(g, p, estride(st), h);
     reconstruct<D, R0, R1, Q0, Q1>(acc, g);
   }
 }
@@ -250,16 +257,16 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
 template <int D, int EPI>
 __device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const double2 (&acc)[4][D],
                                          double (&nrm)[1]) {
-  const long long st = A.g.stride;
-  const double2* __restrict__ x = A.x[par];
-  double2* __restrict__ out = A.out[par];
-  double2* __restrict__ r = A.r[par];
+  const long long st = estride(A.g.stride);
+  const double2* __restrict__ x = A.x[par] ? site_ptr<4 * D>(A.x[par], i) : nullptr;
+  double2* __restrict__ out = A.out[par] ? site_ptr<4 * D>(A.out[par], i) : nullptr;
+  double2* __restrict__ r = A.r[par] ? site_ptr<4 * D>(A.r[par], i) : nullptr;
   double2 xv[4][D], rv[4][D];
 #pragma unroll
   for (int sp = 0; sp < 4; ++sp)
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) {
-      const long long o = (long long)(sp * D + cc) * st + i;
+      const long long o = (long long)(sp * D + cc) * st;
       xv[sp][cc] = x ? ldg(x + o) : make_double2(0.0, 0.0);
       if constexpr (EPI == EPI_CG) rv[sp][cc] = __ldcg(r + o);
     }
@@ -268,7 +275,7 @@ __device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const
   for (int sp = 0; sp < 4; ++sp)
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) {
-      const long long o = (long long)(sp * D + cc) * st + i;
+      const long long o = (long long)(sp * D + cc) * st;
       const double bs = sp < 2 ? A.b : A.b * A.s5acc;
       const double as = sp < 2 ? A.a : A.a * A.s5x;
       double2 v = cscale(bs, acc[sp][cc]);
@@ -331,7 +338,7 @@ __device__ __forceinline__ void pack_site(const PackArgs& P, int j) {
     project<D, G::p0, G::p1, G::f0 ^ 1, G::f1 ^ 1>(h, P.in, st, cb, P.s5in);
     if (MU == 0 && P.bc_kernel && P.t_off + c[0] == P.bc_tlast) negate<D>(h);
     double2 g[2][D];
-    link_mul<D, REAL, FMT, true>(g, link_ptr<D, REAL, FMT>(P.gauge, st, P.in_par, MU, cb), st, h);
+    link_mul<D, REAL, FMT, true>(g, link_ptr<D, REAL, FMT>(P.gauge, st, P.in_par, MU, cb), estride(st), h);
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll

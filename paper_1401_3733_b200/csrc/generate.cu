@@ -248,7 +248,7 @@ struct GenArgs {
   int links;    // LBCU_LINKS_*
   int out_dr;   // entries written per link: N*N (fundamental) or 9 (adjoint)
   int adjoint;  // write the SU(2) adjoint as real links
-  void* out;    // [2][4][out_dr*out_dr][stride] double2 or double
+  void* out;    // [2][4] blocks of out_dr^2 x stride (tiled) double2 or double
   int* bad;
 };
 
@@ -280,11 +280,11 @@ __global__ void k_gauge_generate(const GenArgs A) {
     if (A.adjoint) {
       double r[9];
       if constexpr (N == 2) adjoint_su2(r, u);
-      double* o = static_cast<double*>(A.out) + ((long long)(par * 4 + mu) * 9) * st + cb;
-      for (int e = 0; e < 9; ++e) o[(long long)e * st] = r[e];
+      double* o = site_ptr<9>(static_cast<double*>(A.out) + ((long long)(par * 4 + mu) * 9) * st, cb);
+      for (int e = 0; e < 9; ++e) o[(long long)e * kTile] = r[e];
     } else {
-      double2* o = static_cast<double2*>(A.out) + ((long long)(par * 4 + mu) * N * N) * st + cb;
-      for (int e = 0; e < N * N; ++e) o[(long long)e * st] = u[e];
+      double2* o = site_ptr<N * N>(static_cast<double2*>(A.out) + ((long long)(par * 4 + mu) * N * N) * st, cb);
+      for (int e = 0; e < N * N; ++e) o[(long long)e * kTile] = u[e];
     }
   }
 }
@@ -316,7 +316,7 @@ __global__ void k_spinor_generate(const SpinArgs A) {
                            static_cast<uint64_t>(spin), static_cast<uint64_t>(col)};
     double a, b;
     gauss_pair(key_hash(w), a, b);
-    A.par[p][(long long)k * A.g.stride + cb] = make_double2(a, b);
+    A.par[p][eidx(nv, k, cb)] = make_double2(a, b);
   }
 }
 

@@ -16,7 +16,7 @@ struct lbcu_spinor_s {
   int dr = 0;
   int subset = LBCU_FULL;
   double2* base = nullptr;
-  double2* par[2] = {nullptr, nullptr};  // parity blocks [4 dr][stride]
+  double2* par[2] = {nullptr, nullptr};  // parity blocks of 4 dr x stride elements, 32-site tiles
   size_t elems = 0;                      // double2 elements over present parities
   bool has(int p) const { return par[p] != nullptr; }
 };

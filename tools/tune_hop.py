@@ -25,9 +25,12 @@ def main():
     ap.add_argument("--sweep", action="append", default=[], help="NAME=v1,v2,...")
     ap.add_argument("--dense-links", action="store_true")
     ap.add_argument("--fundamental", action="store_true", help="upload fundamental links (SU(4) AS)")
+    ap.add_argument("--lattice", default=None, help="T,X,Y,Z overriding the config's lattice")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     L, n, rep, mass = cfg["L"], cfg["n"], cfg["rep"], cfg["mass"]
+    if args.lattice:
+        L = [int(v) for v in args.lattice.split(",")]
     dr = lb.rep_dim(rep, n)
     real = lb.rep_is_real(rep)
     links = {"haar": lb.LINKS_HAAR, "near_unit": lb.LINKS_NEAR_UNIT}[cfg["links"]]
