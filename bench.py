@@ -368,7 +368,8 @@ def run_gpu(args, cfg):
                          "kernels_per_step": kernels_per_step,
                          "traffic": traffic_from_profiles(f"cfg{args.config}_dphi_{fmt}"),
                          "eo_hop": {"ms": hop_ms, "achieved": hop_gbs, "frac": hop_gbs / peak,
-                                    "bytes_per_output_site": bytes_eo_hop(dr, real, fmt)}},
+                                    "bytes_per_output_site": bytes_eo_hop(dr, real, fmt),
+                                    "traffic": traffic_from_profiles(f"cfg{args.config}_hop_{fmt}")}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,

@@ -17,9 +17,10 @@ def main(path, title):
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
         v = float(r["Metric Value"].replace(",", ""))
-        if r.get("Metric Unit") == "nsecond":
+        unit = r.get("Metric Unit")
+        if unit in ("ns", "nsecond"):
             v /= 1e3
-        elif r.get("Metric Unit") == "msecond":
+        elif unit in ("ms", "msecond"):
             v *= 1e3
         tot[r["Kernel Name"]] += v
         cnt[r["Kernel Name"]] += 1

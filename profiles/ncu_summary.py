@@ -30,8 +30,9 @@ def main(path):
             rd = float(r[hdr.index("dram__bytes_read.sum")])
             wr = float(r[hdr.index("dram__bytes_write.sum")])
             mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            u = units[hdr.index("dram__bytes_read.sum")]
-            print(f"  {'traffic (read+write) bytes':70s} {(rd + wr) * mul.get(u, 1):16.4e}")
+            ur = mul.get(units[hdr.index("dram__bytes_read.sum")], 1)
+            uw = mul.get(units[hdr.index("dram__bytes_write.sum")], 1)
+            print(f"  {'traffic (read+write) bytes':70s} {rd * ur + wr * uw:16.4e}")
 
 
 if __name__ == "__main__":
