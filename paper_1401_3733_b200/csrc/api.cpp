@@ -264,7 +264,7 @@ int lbcu_ctx_create(lbcu_world w, int rank, int device, const int global[4], con
   LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
   LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_comm, cudaEventDisableTiming));
   for (auto& e : ctx->ev) LBCU_CUDA(cudaEventCreate(&e));
-  ctx->max_partials = static_cast<int>(2 * ((g.vh + 127) / 128) + 4096);
+  ctx->max_partials = static_cast<int>(2 * ((g.vh + 31) / 32) + 4096);  // hop blocks >= 32 threads
   LBCU_CUDA(cudaMalloc(&ctx->partials, sizeof(double) * 2 * ctx->max_partials));
   LBCU_CUDA(cudaMalloc(&ctx->ticket, sizeof(unsigned) * 4));
   LBCU_CUDA(cudaMemset(ctx->ticket, 0, sizeof(unsigned) * 4));

@@ -239,7 +239,6 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
     for (int k = 0; k < 4; ++k)
 #pragma unroll
       for (int cc = 0; cc < D; ++cc) acc[k][cc] = make_double2(0.0, 0.0);
-    const long long st = A.g.stride;
     const double2* in = A.in[par ^ 1];
     hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
     hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
@@ -358,7 +357,7 @@ __global__ void __launch_bounds__(128) pack_kernel(const __grid_constant__ PackA
   }
 }
 
-constexpr int kBlock = 128;
+constexpr int kBlock = 128;  // launch-bounds block size (pack kernel, upper bound)
 
 // Occupancy knob: LBCU_HOP_MINB = minimum resident 128-thread blocks per SM
 // requested from ptxas (__launch_bounds__), i.e. a register cap.
@@ -378,13 +377,23 @@ int default_minb() {
   return 1;
 }
 
-int hop_blocks(int nsites, int npar, int /*dr*/) { return (nsites + kBlock - 1) / kBlock * npar; }
+// hop block size (<= kBlock); LBCU_HOP_BLOCK=64 halves it (finer scheduling)
+int hop_block() {
+  static const int b = [] {
+    const char* e = std::getenv("LBCU_HOP_BLOCK");
+    const int v = e ? std::atoi(e) : kBlock;
+    return (v == 32 || v == 64) ? v : kBlock;
+  }();
+  return b;
+}
+
+int hop_blocks(int nsites, int npar, int /*dr*/) { return (nsites + hop_block() - 1) / hop_block() * npar; }
 
 template <int D, bool REAL, int FMT, int MINB>
 void launch_hop_minb(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream_t s) {
 #define LBCU_HOP_CASE(B, E)                                                         \
   if (bnd == B && epi == E) {                                                       \
-    hop_kernel<D, REAL, FMT, B, E, MINB><<<blocks, kBlock, 0, s>>>(A);              \
+    hop_kernel<D, REAL, FMT, B, E, MINB><<<blocks, hop_block(), 0, s>>>(A);         \
     return;                                                                         \
   }
   LBCU_HOP_CASE(false, EPI_STORE)
@@ -527,7 +536,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       if (bx < geo.local[1]) {  // a whole slice fits: the linear order is the same sweep
         A.sched_bx = bx;
         A.sched_len = bx * geo.local[2] * geo.local[3] / 2;
-        A.sched_cpb = (A.sched_len + kBlock - 1) / kBlock;
+        A.sched_cpb = (A.sched_len + hop_block() - 1) / hop_block();
         blocks = (geo.local[1] / bx) * geo.local[0] * A.sched_cpb * npar;
       }
     }

@@ -14,6 +14,10 @@
 //             - 2 a0 eps_abc a_c with al = a0 + i a3, be = a2 + i a1
 //             (group.cpp:126-143 convention, checked in tests/test_host.py)
 //   GF_R12  : SU(3) rows 0 and 1 (6 complex); row 2 = conj(row0 x row1)
+//   GF_AS4  : two-index antisymmetric rep of SU(4) (dr = 6) stored as the
+//             fundamental 4 x 4 element (16 complex instead of 36); entries
+//             R_(ij),(kl) = u_ik u_jl - u_il u_jk (group.cpp:146-158) are
+//             formed in registers. Uploaded through lbcu_gauge_upload_fundamental.
 //
 // Compact formats are chosen at upload only when every link reconstructs to
 // within 1e-12 of the uploaded matrix (gauge.cu), so arbitrary user links
@@ -28,10 +32,14 @@
 
 namespace lbcu {
 
-//   GF_AS4  : two-index antisymmetric rep of SU(4) (dr = 6) stored as the
-//             fundamental 4 x 4 element (16 complex instead of 36); entries
-//             R_(ij),(kl) = u_ik u_jl - u_il u_jk (group.cpp:146-158) are
-//             formed in registers. Uploaded through lbcu_gauge_upload_fundamental.
+// Link loads: the read-only path. (L1::no_allocate hints, to leave L1 to the
+// neighbour spinors, measured 0-8 % slower: the full Dphi's two parities
+// share links through L1.)
+template <class T>
+__device__ __forceinline__ T ldlink(const T* p) {
+  return __ldg(p);
+}
+
 enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2, GF_AS4 = 3 };
 
 template <bool REAL>
@@ -105,11 +113,11 @@ __device__ __forceinline__ void load_link(LinkT<REAL> (&u)[D * D],
                                           long long st) {
   if constexpr (FMT == GF_FULL) {
 #pragma unroll
-    for (int e = 0; e < D * D; ++e) u[e] = __ldg(p + (long long)e * st);
+    for (int e = 0; e < D * D; ++e) u[e] = ldlink(p + (long long)e * st);
   } else {
     double2 s[LinkFmt<D, REAL, FMT>::entries];
 #pragma unroll
-    for (int e = 0; e < LinkFmt<D, REAL, FMT>::entries; ++e) s[e] = __ldg(p + (long long)e * st);
+    for (int e = 0; e < LinkFmt<D, REAL, FMT>::entries; ++e) s[e] = ldlink(p + (long long)e * st);
     build_link<D, REAL, FMT>(u, s);
   }
 }
@@ -127,7 +135,7 @@ __device__ __forceinline__ void link_mul(double2 (&g)[2][D],
     for (int r = 0; r < D; ++r)
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const auto u = __ldg(p + (long long)(DAG ? c * D + r : r * D + c) * st);
+        const auto u = ldlink(p + (long long)(DAG ? c * D + r : r * D + c) * st);
         if constexpr (REAL) {
           rmac(g[0][r], u, h[0][c]);
           rmac(g[1][r], u, h[1][c]);
@@ -173,7 +181,7 @@ __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
     // keep only the fundamental element in registers; form each minor when used
     double2 s[16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) s[e] = __ldg(p + (long long)e * st);
+    for (int e = 0; e < 16; ++e) s[e] = ldlink(p + (long long)e * st);
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
       double2 g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
@@ -207,7 +215,7 @@ __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
     for (int c = 0; c < D; ++c) {
       const int idx = DAG ? c * D + r : r * D + c;
       LinkT<REAL> e;
-      if constexpr (FMT == GF_FULL) e = __ldg(p + (long long)idx * st);
+      if constexpr (FMT == GF_FULL) e = ldlink(p + (long long)idx * st);
       else e = u[idx];
       if constexpr (REAL) {
         rmac(g0, e, h[0][c]);
