@@ -141,25 +141,30 @@ int lbcu_gauge_download(lbcu_gauge g, double* host); /* as uploaded (no BC sign)
  * uploaded link reconstructs to within 1e-12 (checked at upload):
  *   LBCU_GAUGE_SU2 : SU(2) links as 2 complex (fundamental; adjoint rebuilt)
  *   LBCU_GAUGE_R12 : SU(3) fundamental, two rows (third = conj(r0 x r1))
+ *   LBCU_GAUGE_AS4R: SU(4) antisymmetric as a real SO(6) matrix in a fixed
+ *                    real basis of the 6 (the kernels rotate colour vectors)
  * otherwise LBCU_GAUGE_FULL (dense dr x dr). set_compact(0) before upload
  * forces dense storage. */
 enum lbcu_gauge_format {
   LBCU_GAUGE_FULL = 0,
   LBCU_GAUGE_SU2 = 1,
   LBCU_GAUGE_R12 = 2,
-  LBCU_GAUGE_AS4 = 3 /* SU(4) antisymmetric formed from fundamental links */
+  LBCU_GAUGE_AS4 = 3, /* SU(4) antisymmetric formed from fundamental links */
+  LBCU_GAUGE_AS4R = 4 /* SU(4) antisymmetric, real basis (36 doubles) */
 };
 int lbcu_gauge_set_compact(lbcu_gauge g, int enable);
 /* Upload the FUNDAMENTAL SU(N) links (host layout [site][mu][N][N] complex,
  * the group elements randomize_gauge_interior draws before represent(),
  * fields.cpp:95-96); the represented link is formed on the fly in the
  * kernels. Supported for the SU(4) antisymmetric representation (BASELINE
- * config 5): 16 instead of 36 complex numbers per link. */
+ * config 5): stored as LBCU_GAUGE_AS4R when every element is in SU(4) to
+ * 1e-12, else as the 16 fundamental entries (LBCU_GAUGE_AS4; also forced by
+ * the environment variable LBCU_AS4_STORAGE=fund). */
 int lbcu_gauge_upload_fundamental(lbcu_gauge g, const double* host_fundamental);
 /* init_gauge_random on the device: the keyed generators of
  * fields.cpp:86-107 / group.cpp:82-114 evaluated per link on the GPU
- * (fundamental SU(2..4), the SU(2) adjoint, SU(4) antisymmetric via AS4
- * storage; links = UNIT / HAAR / NEAR_UNIT). Agrees with the host generator
+ * (fundamental SU(2..4), the SU(2) adjoint, SU(4) antisymmetric via
+ * AS4R / AS4 storage; links = UNIT / HAAR / NEAR_UNIT). Agrees with the host generator
  * to a few ulp (device transcendentals). */
 int lbcu_gauge_generate(lbcu_gauge g, int links, uint64_t seed, double eps);
 /* init_spinor_random (fields.cpp:22-40) on the device */

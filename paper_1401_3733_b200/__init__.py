@@ -404,7 +404,7 @@ class GaugeField:
         """(format name, max reconstruction error at the last upload)."""
         f, e = C.c_int(), C.c_double()
         _check(lib().lbcu_gauge_storage(self._h, C.byref(f), C.byref(e)))
-        return {0: "full", 1: "su2", 2: "r12", 3: "as4"}[f.value], e.value
+        return {0: "full", 1: "su2", 2: "r12", 3: "as4", 4: "as4r"}[f.value], e.value
 
     def download(self) -> np.ndarray:
         dt = np.float64 if self.real_links else np.complex128

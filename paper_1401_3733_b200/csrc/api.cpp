@@ -439,12 +439,8 @@ int lbcu_gauge_generate(lbcu_gauge g, int links, uint64_t seed, double eps) {
   lbcu_ctx_s* c = g->ctx;
   bind(c);
   if (g->rep == LBCU_REP_ANTISYMMETRIC && g->n == 4 && g->compact_ok) {
-    // fundamental elements are the AS4 storage itself
-    void* fund = gauge_generate_dense(c, g, links, seed, eps, true);
-    if (g->base) LBCU_CUDA(cudaFree(g->base));
-    g->base = fund;
-    g->fmt = 3;  // GF_AS4
-    g->compact_err = 0.0;
+    // SU(4) fundamental elements -> real SO(6) storage (or kept as AS4)
+    gauge_adopt_fundamental(c, g, gauge_generate_dense(c, g, links, seed, eps, true));
   } else {
     gauge_adopt_dense(c, g, gauge_generate_dense(c, g, links, seed, eps, false));
   }

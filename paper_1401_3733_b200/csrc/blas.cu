@@ -440,10 +440,13 @@ int compact_format(const lbcu_gauge_s* g) {
   if (g->dr == 2 && !g->real) return GF_SU2;  // SU(2) fundamental
   if (g->dr == 3 && g->real && g->n == 2) return GF_SU2;  // SU(2) adjoint
   if (g->dr == 3 && !g->real && g->n == 3 && g->rep == LBCU_REP_FUNDAMENTAL) return GF_R12;
+  if (g->dr == 6 && !g->real && g->n == 4 && g->rep == LBCU_REP_ANTISYMMETRIC) return GF_AS4R;
   return GF_FULL;
 }
 
-int fmt_entries(int fmt, int dr) { return fmt == GF_SU2 ? 2 : fmt == GF_R12 ? 6 : dr * dr; }
+int fmt_entries(int fmt, int dr) {
+  return fmt == GF_SU2 ? 2 : fmt == GF_R12 ? 6 : fmt == GF_AS4 ? 16 : fmt == GF_AS4R ? 18 : dr * dr;
+}
 
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double v) {
   atomicMax(p, __double_as_longlong(v));  // non-negative doubles order like their bit patterns
@@ -497,6 +500,8 @@ __global__ void k_compress(const LinkT<REAL>* __restrict__ full, double2* __rest
       }
       st[0] = make_double2(w, -vz);   // al = a0 + i a3
       st[1] = make_double2(-vy, -vx); // be = a2 + i a1
+    } else if constexpr (FMT == GF_AS4R) {
+      as4r_from_dense(u, st);  // imaginary residue caught by the rebuild check below
     } else {
 #pragma unroll
       for (int e = 0; e < 6; ++e) st[e] = u[e];
@@ -513,6 +518,27 @@ __global__ void k_compress(const LinkT<REAL>* __restrict__ full, double2* __rest
       else d = sqrt(cabs2(make_double2(r[e].x - u[e].x, r[e].y - u[e].y)));
       worst = fmax(worst, d);
     }
+  }
+  if (worst > 0.0 || !isfinite(worst)) atomic_max_nonneg(err, isfinite(worst) ? worst : 1e300);
+}
+
+// SU(4) fundamental elements -> GF_AS4R (minors, then the real basis);
+// err = max |Im R'| (non-zero only for non-SU(4) input)
+__global__ void k_as4r_from_fund(const double2* __restrict__ fund, double2* __restrict__ compact,
+                                 long long stride, int vh, unsigned long long* err) {
+  const long long n = 8LL * vh;
+  double worst = 0.0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const long long blk = t / vh, cb = t % vh;
+    double2 s[16], u[36], st[18];
+    const double2* f = site_ptr<16>(fund + blk * 16 * stride, cb);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) s[e] = f[(long long)e * kTile];
+    build_link<6, false, GF_AS4>(u, s);
+    worst = fmax(worst, as4r_from_dense(u, st));
+    double2* cp = site_ptr<18>(compact + blk * 18 * stride, cb);
+#pragma unroll
+    for (int e = 0; e < 18; ++e) cp[(long long)e * kTile] = st[e];
   }
   if (worst > 0.0 || !isfinite(worst)) atomic_max_nonneg(err, isfinite(worst) ? worst : 1e300);
 }
@@ -559,6 +585,8 @@ void dispatch_compact(const lbcu_gauge_s* g, int fmt, F&& f) {
     return f(integral_constant<int, 3>{}, std::true_type{}, integral_constant<int, GF_SU2>{});
   if (fmt == GF_R12)
     return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_R12>{});
+  if (fmt == GF_AS4R)
+    return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_AS4R>{});
   throw Error(LBCU_CONTRACT_VIOLATION, "no compact gauge format");
 }
 
@@ -681,11 +709,48 @@ void gauge_upload_fundamental(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* ho
   double2* b = static_cast<double2*>(base);
   launch_to_soa<double2>(ctx, static_cast<const double2*>(ctx->staging), b,
                          b + static_cast<size_t>(nv) * geo.stride, nv, 0, 16);
-  LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (g->base) LBCU_CUDA(cudaFree(g->base));
-  g->base = base;
+  gauge_adopt_fundamental(ctx, g, base);
+}
+
+// Take ownership of tiled SU(4) fundamental links [2][4] x 16 entries:
+// store them as real SO(6) matrices (GF_AS4R) when every link is SU(4) to
+// 1e-12, else keep the fundamental elements (GF_AS4, exact for any input).
+// LBCU_AS4_STORAGE=fund keeps GF_AS4.
+void gauge_adopt_fundamental(lbcu_ctx_s* ctx, lbcu_gauge_s* g, void* fund) {
+  const Geometry& geo = ctx->geo;
+  const char* env = std::getenv("LBCU_AS4_STORAGE");
+  const bool want_real = compaction_enabled(g) && !(env && std::string(env) == "fund");
+  if (g->base && g->base != fund) LBCU_CUDA(cudaFree(g->base));
+  g->base = fund;
   g->fmt = GF_AS4;
   g->compact_err = 0.0;
+  if (want_real) {
+    const size_t cbytes = 2 * 4 * 18 * static_cast<size_t>(geo.stride) * sizeof(double2);
+    void* compact = nullptr;
+    LBCU_CUDA(cudaMalloc(&compact, cbytes));
+    LBCU_CUDA(cudaMemsetAsync(compact, 0, cbytes, ctx->stream));
+    unsigned long long* derr = reinterpret_cast<unsigned long long*>(ctx->dscal + 60);
+    LBCU_CUDA(cudaMemsetAsync(derr, 0, sizeof(unsigned long long), ctx->stream));
+    k_as4r_from_fund<<<grid_for(8LL * geo.vh), 256, 0, ctx->stream>>>(
+        static_cast<const double2*>(fund), static_cast<double2*>(compact), geo.stride,
+        static_cast<int>(geo.vh), derr);
+    ctx->launches++;
+    LBCU_CUDA(cudaGetLastError());
+    unsigned long long bits = 0;
+    LBCU_CUDA(cudaMemcpyAsync(&bits, derr, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream));
+    LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+    double err;
+    std::memcpy(&err, &bits, sizeof(err));
+    if (err <= 1e-12) {
+      LBCU_CUDA(cudaFree(fund));
+      g->base = compact;
+      g->fmt = GF_AS4R;
+      g->compact_err = err;
+    } else {
+      LBCU_CUDA(cudaFree(compact));
+    }
+  }
+  LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host) {

@@ -131,7 +131,7 @@ __device__ __forceinline__ const ElemT<D, REAL, FMT>* link_ptr(const void* gauge
 template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
 __device__ __forceinline__ void link_hop(double2 (&acc)[4][D], const ElemT<D, REAL, FMT>* p,
                                          long long st, const double2 (&h)[2][D]) {
-  if constexpr (D <= 3 || FMT == GF_AS4) {
+  if constexpr (D <= 3 || FMT == GF_AS4 || FMT == GF_AS4R) {
     link_mul_acc<D, REAL, FMT, DAG, R0, R1, Q0, Q1>(acc, p, estride(st), h);
   } else {
     double2 g[2][D];
@@ -184,7 +184,14 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int cc = 0; cc < D; ++cc) g[a][cc] = ldg(A.hbwd[MU] + (a * D + cc) * hc + j);
-      reconstruct<D, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, g);
+      if constexpr (FMT == GF_AS4R) {  // halo records are in the standard basis
+        double2 t[2][D];
+        as4r_in(t[0], g[0]);
+        as4r_in(t[1], g[1]);
+        reconstruct<D, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, t);
+      } else {
+        reconstruct<D, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, g);
+      }
     } else {
       double2 h[2][D];
       const int nb = nb_bwd(A.g, s, c, MU) >> 1;
@@ -244,6 +251,10 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
     hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
     hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
     hop_mu<D, REAL, FMT, BND, 3>(acc, A, in, par, i, s, c);
+    if constexpr (FMT == GF_AS4R) {  // back from the real-basis colour frame
+#pragma unroll
+      for (int sp = 0; sp < 4; ++sp) as4r_out(acc[sp], 0.5);
+    }
 
     epilogue<D, EPI>(A, par, i, acc, nrm);
   }
@@ -447,6 +458,7 @@ void dispatch(int dr, bool real, int fmt, F&& f) {
       case 4: return f(integral_constant<int, 4>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
       case 6:
         if (fmt == GF_AS4) return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_AS4>{});
+        if (fmt == GF_AS4R) return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_AS4R>{});
         return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
       case 10: return f(integral_constant<int, 10>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
     }
@@ -526,7 +538,8 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     // L2-blocked schedule: spatial blocks of bx x-planes whose two-slice
     // working set (spinor in/out + links as stored) fits the L2 budget
     if (env_int("LBCU_HOP_SCHED", 1)) {
-      const int lb = fmt == GF_SU2 ? 32 : fmt == GF_R12 ? 96 : fmt == GF_AS4 ? 256 : dr * dr * (real ? 8 : 16);
+      const int lb = fmt == GF_SU2 ? 32 : fmt == GF_R12 ? 96 : fmt == GF_AS4 ? 256 : fmt == GF_AS4R ? 288
+                                                                                    : dr * dr * (real ? 8 : 16);
       const double site_bytes = 128.0 * dr + (npar == 2 ? 4 : 8) * lb;
       const double plane_bytes = site_bytes * geo.local[2] * geo.local[3];
       const double budget = env_int("LBCU_HOP_L2MB", 32) * 1e6;

@@ -18,6 +18,16 @@
 //             fundamental 4 x 4 element (16 complex instead of 36); entries
 //             R_(ij),(kl) = u_ik u_jl - u_il u_jk (group.cpp:146-158) are
 //             formed in registers. Uploaded through lbcu_gauge_upload_fundamental.
+//   GF_AS4R : the same representation as a REAL SO(6) matrix. The 6 of SU(4)
+//             is a real representation: in the basis B whose columns are
+//             s(e_a + g e_b), i s(e_a - g e_b) for the complementary index
+//             pairs (01|23, g=+1), (02|13, g=-1), (03|12, g=+1), s = 1/sqrt2,
+//             R' = B^dag R B is real orthogonal (36 doubles = 288 B, stored as
+//             18 double2). Kernels carry colour vectors in Wt = sqrt2 B^dag:
+//             Wt (R h) = R' (Wt h), so h is rotated per hop (12 adds), the
+//             multiply is real x complex (a quarter of the FP64 work of the
+//             AS4 minors), and the accumulator is rotated back once per site,
+//             acc = 1/2 Wt^dag acc'.
 //
 // Compact formats are chosen at upload only when every link reconstructs to
 // within 1e-12 of the uploaded matrix (gauge.cu), so arbitrary user links
@@ -40,7 +50,7 @@ __device__ __forceinline__ T ldlink(const T* p) {
   return __ldg(p);
 }
 
-enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2, GF_AS4 = 3 };
+enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2, GF_AS4 = 3, GF_AS4R = 4 };
 
 template <bool REAL>
 using LinkT = std::conditional_t<REAL, double, double2>;
@@ -48,9 +58,9 @@ using LinkT = std::conditional_t<REAL, double, double2>;
 template <int D, bool REAL, int FMT>
 struct LinkFmt {
   static constexpr bool valid = FMT == GF_FULL || (FMT == GF_SU2 && ((D == 2 && !REAL) || (D == 3 && REAL))) ||
-                                (FMT == GF_R12 && D == 3 && !REAL) || (FMT == GF_AS4 && D == 6 && !REAL);
+                                (FMT == GF_R12 && D == 3 && !REAL) || ((FMT == GF_AS4 || FMT == GF_AS4R) && D == 6 && !REAL);
   static constexpr int entries =
-      FMT == GF_FULL ? D * D : (FMT == GF_SU2 ? 2 : (FMT == GF_R12 ? 6 : 16));
+      FMT == GF_FULL ? D * D : (FMT == GF_SU2 ? 2 : (FMT == GF_R12 ? 6 : (FMT == GF_AS4 ? 16 : 18)));
   using Elem = std::conditional_t<FMT == GF_FULL, LinkT<REAL>, double2>;
 };
 
@@ -63,6 +73,77 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+// ---- GF_AS4R basis (see header) --------------------------------------------
+// pair k = 0, 1, 2 couples colour indices a = k and b = 5 - k with sign g
+__host__ __device__ constexpr double as4r_sign(int k) { return k == 1 ? -1.0 : 1.0; }
+
+// B[i][x] (unitary, columns = real basis vectors)
+__device__ __forceinline__ double2 as4r_B(int i, int x) {
+  constexpr double s = 0.70710678118654752440;
+  const int k = x >> 1, a = k, b = 5 - k;
+  const double g = as4r_sign(k);
+  if (i != a && i != b) return make_double2(0.0, 0.0);
+  if (x & 1) return i == a ? make_double2(0.0, s) : make_double2(0.0, -g * s);
+  return make_double2(i == a ? s : g * s, 0.0);
+}
+
+// R' = B^dag R B from a dense AS link; returns max |Im R'| (0 for SU(4))
+__device__ __forceinline__ double as4r_from_dense(const double2 (&u)[36], double2 (&st)[18]) {
+  double worst = 0.0;
+#pragma unroll
+  for (int x = 0; x < 6; ++x) {
+    double row[6];
+#pragma unroll
+    for (int y = 0; y < 6; ++y) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double2 bi = as4r_B(i, x);
+        if (bi.x == 0.0 && bi.y == 0.0) continue;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const double2 bj = as4r_B(j, y);
+          if (bj.x == 0.0 && bj.y == 0.0) continue;
+          const double2 t = cmul(cmul(cconj(bi), u[i * 6 + j]), bj);
+          acc.x += t.x;
+          acc.y += t.y;
+        }
+      }
+      row[y] = acc.x;
+      worst = fmax(worst, fabs(acc.y));
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) st[3 * x + q] = make_double2(row[2 * q], row[2 * q + 1]);
+  }
+  return worst;
+}
+
+// o = Wt h = sqrt2 B^dag h
+__device__ __forceinline__ void as4r_in(double2 (&o)[6], const double2 (&h)[6]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double g = as4r_sign(k);
+    const double2 ha = h[k], hb = h[5 - k];
+    o[2 * k] = make_double2(fma(g, hb.x, ha.x), fma(g, hb.y, ha.y));
+    const double2 d = make_double2(fma(-g, hb.x, ha.x), fma(-g, hb.y, ha.y));
+    o[2 * k + 1] = make_double2(d.y, -d.x);  // -i d
+  }
+}
+
+// v <- scale * Wt^dag v, Wt^dag = sqrt2 B
+__device__ __forceinline__ void as4r_out(double2 (&v)[6], double scale) {
+  double2 w[6];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double g = as4r_sign(k);
+    const double2 p = v[2 * k], q = v[2 * k + 1];
+    w[k] = make_double2(scale * (p.x - q.y), scale * (p.y + q.x));          // p + i q
+    w[5 - k] = make_double2(g * scale * (p.x + q.y), g * scale * (p.y - q.x));  // g (p - i q)
+  }
+#pragma unroll
+  for (int c = 0; c < 6; ++c) v[c] = w[c];
+}
 
 // Rebuild the represented link (row-major D x D) from compact entries.
 template <int D, bool REAL, int FMT>
@@ -95,6 +176,29 @@ __device__ __forceinline__ void build_link(LinkT<REAL> (&u)[D * D],
     u[6] = cconj(csub(cmul(u[1], u[5]), cmul(u[2], u[4])));
     u[7] = cconj(csub(cmul(u[2], u[3]), cmul(u[0], u[5])));
     u[8] = cconj(csub(cmul(u[0], u[4]), cmul(u[1], u[3])));
+  } else if constexpr (FMT == GF_AS4R) {  // R = B R' B^dag
+    double m[36];
+#pragma unroll
+    for (int e = 0; e < 18; ++e) {
+      m[2 * e] = s[e].x;
+      m[2 * e + 1] = s[e].y;
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int x = 0; x < 6; ++x)
+#pragma unroll
+          for (int y = 0; y < 6; ++y) {
+            const double2 bx = as4r_B(i, x), by = cconj(as4r_B(j, y));
+            const double2 t = cmul(bx, by);
+            acc.x = fma(m[x * 6 + y], t.x, acc.x);
+            acc.y = fma(m[x * 6 + y], t.y, acc.y);
+          }
+        u[i * 6 + j] = acc;
+      }
   } else {  // GF_AS4: all 36 minors of the fundamental element
 #pragma unroll
     for (int p = 0; p < 6; ++p)
@@ -122,11 +226,49 @@ __device__ __forceinline__ void load_link(LinkT<REAL> (&u)[D * D],
   }
 }
 
+// GF_AS4R: g' = M hp with M = R' (or R'^T for the dagger), all in the Wt
+// basis; the link is streamed one stored row (3 double2) at a time.
+template <bool DAG>
+__device__ __forceinline__ void as4r_mul(double2 (&g)[2][6], const double2* __restrict__ p, long long st,
+                                         const double2 (&hp)[2][6]) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r) g[0][r] = g[1][r] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    double m[6];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double2 v = ldlink(p + (long long)(3 * r + q) * st);
+      m[2 * q] = v.x;
+      m[2 * q + 1] = v.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      if constexpr (DAG) {  // g[c] += R'_rc hp[r]
+        rmac(g[0][c], m[c], hp[0][r]);
+        rmac(g[1][c], m[c], hp[1][r]);
+      } else {  // g[r] += R'_rc hp[c]
+        rmac(g[0][r], m[c], hp[0][c]);
+        rmac(g[1][r], m[c], hp[1][c]);
+      }
+    }
+  }
+}
+
 // g[a][r] = sum_c M_rc h[a][c] with M = U (DAG = false) or U^dag (DAG = true)
 template <int D, bool REAL, int FMT, bool DAG>
 __device__ __forceinline__ void link_mul(double2 (&g)[2][D],
                                          const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
                                          long long st, const double2 (&h)[2][D]) {
+  if constexpr (FMT == GF_AS4R) {  // result in the standard basis
+    double2 hp[2][6];
+    as4r_in(hp[0], h[0]);
+    as4r_in(hp[1], h[1]);
+    as4r_mul<DAG>(g, p, st, hp);
+    as4r_out(g[0], 0.5);
+    as4r_out(g[1], 0.5);
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < D; ++r) g[0][r] = g[1][r] = make_double2(0.0, 0.0);
   if constexpr (FMT == GF_FULL) {
@@ -177,6 +319,20 @@ template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
 __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
                                              const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
                                              long long st, const double2 (&h)[2][D]) {
+  if constexpr (FMT == GF_AS4R) {  // acc in the Wt basis (site_body rotates back)
+    double2 hp[2][6], g[2][6];
+    as4r_in(hp[0], h[0]);
+    as4r_in(hp[1], h[1]);
+    as4r_mul<DAG>(g, p, st, hp);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      acc[0][r] = cadd(acc[0][r], g[0][r]);
+      acc[1][r] = cadd(acc[1][r], g[1][r]);
+      acc[2][r] = cadd(acc[2][r], phm<Q0>(g[R0][r]));
+      acc[3][r] = cadd(acc[3][r], phm<Q1>(g[R1][r]));
+    }
+    return;
+  }
   if constexpr (FMT == GF_AS4) {
     // keep only the fundamental element in registers; form each minor when used
     double2 s[16];

@@ -132,6 +132,7 @@ void gauge_upload(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host);
 void gauge_download(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double* host);
 void gauge_upload_fundamental(lbcu_ctx_s* ctx, lbcu_gauge_s* g, const double* host);
 void gauge_adopt_dense(lbcu_ctx_s* ctx, lbcu_gauge_s* g, void* full);
+void gauge_adopt_fundamental(lbcu_ctx_s* ctx, lbcu_gauge_s* g, void* fund);
 // on-device keyed generation (generate.cu)
 void spinor_generate(lbcu_ctx_s* ctx, lbcu_spinor_s* s, uint64_t seed, uint64_t field);
 void* gauge_generate_dense(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, int links, uint64_t seed,

@@ -28,7 +28,7 @@ def test_spinor_generate_matches_host(dr):
     (3, lb.FUNDAMENTAL, lb.LINKS_HAAR, "r12"),
     (3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT, "r12"),
     (2, lb.ADJOINT, lb.LINKS_HAAR, "su2"),
-    (4, lb.ANTISYMMETRIC, lb.LINKS_HAAR, "as4"),
+    (4, lb.ANTISYMMETRIC, lb.LINKS_HAAR, "as4r"),
     (4, lb.FUNDAMENTAL, lb.LINKS_HAAR, "full"),
     (3, lb.FUNDAMENTAL, lb.LINKS_UNIT, "r12"),
 ], ids=["su2f", "su3f", "su3f-near-unit", "su2a", "su4as", "su4f", "unit"])

@@ -281,7 +281,7 @@ def test_near_unit_links_cg_eo():
     (2, lb.ADJOINT, lb.LINKS_HAAR, "su2"),
     (3, lb.FUNDAMENTAL, lb.LINKS_HAAR, "r12"),
     (3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT, "r12"),
-    (4, lb.ANTISYMMETRIC, lb.LINKS_HAAR, "full"),
+    (4, lb.ANTISYMMETRIC, lb.LINKS_HAAR, "as4r"),
 ], ids=["su2f", "su2a", "su3f", "su3f-near-unit", "su4as"])
 @pytest.mark.parametrize("bc", [lb.PERIODIC, lb.ANTIPERIODIC_T], ids=["periodic", "antiperiodic"])
 def test_compact_link_storage_is_exact(n, rep, links, fmt, bc):
