@@ -379,12 +379,11 @@ int env_int(const char* name, int dflt) {
 
 template <int D, bool REAL, int FMT>
 int default_minb() {
-  // profiles/r01_tune_*: a cap of 3 blocks/SM helps D = 2 (13 % with SU(2)
-  // links) and the real adjoint; dense/R12 SU(3) runs best uncapped on the eo
-  // hop; larger D spill under any cap.
-  if (D == 2 && FMT == GF_SU2) return 4;  // r01_tune_minb_su2 (1 % over 3)
-  if (D == 2 || (D == 3 && REAL)) return 3;
-  if (D == 3 && FMT == GF_FULL) return 3;
+  // profiles/r01_tune_minb_*, r02 (tiled layout): 4 blocks/SM for the compact
+  // SU(2) links (fundamental and adjoint, 2-4 %), 3 for the other dr <= 3
+  // formats (R12 1 %, dense); larger dr spill under any cap.
+  if (FMT == GF_SU2) return 4;
+  if (D <= 3) return 3;
   return 1;
 }
 
@@ -423,11 +422,11 @@ void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaS
   const int blocks = blocks_override > 0 ? blocks_override : hop_blocks(nsites, npar, D);
   if constexpr (D <= 3) {
     const int minb = env_int("LBCU_HOP_MINB", default_minb<D, REAL, FMT>());
+    if (minb == 4) {
+      launch_hop_minb<D, REAL, FMT, 4>(A, bnd, epi, blocks, s);
+      return;
+    }
     if constexpr (D == 2 && FMT == GF_SU2) {
-      if (minb == 4) {
-        launch_hop_minb<D, REAL, FMT, 4>(A, bnd, epi, blocks, s);
-        return;
-      }
       if (minb == 5) {
         launch_hop_minb<D, REAL, FMT, 5>(A, bnd, epi, blocks, s);
         return;
