@@ -315,6 +315,27 @@ def run_gpu(args, cfg):
     got = hout[(e2e_steps - 1) % 2].numpy().view(np.complex128).reshape(s.shape)
     lb.apply_dirac(b, gauge, a, mass)
     e2e_err = float(np.linalg.norm(got - b.download()) / np.linalg.norm(got))
+    # the bound of this number: concurrent pinned H2D + D2H of the same bytes
+    # (the copies the pipeline overlaps), plain cudaMemcpyAsync on two streams
+    dbuf = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    sh, sd = torch.cuda.Stream(), torch.cuda.Stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    torch.cuda.synchronize()
+    t0.record()
+    sh.wait_event(t0)
+    sd.wait_event(t0)
+    for k in range(reps):
+        with torch.cuda.stream(sh):
+            dbuf[0].copy_(hin[k % 2], non_blocking=True)
+        with torch.cuda.stream(sd):
+            hout[k % 2].copy_(dbuf[1], non_blocking=True)
+    torch.cuda.current_stream().wait_stream(sh)
+    torch.cuda.current_stream().wait_stream(sd)
+    t1.record()
+    torch.cuda.synchronize()
+    duplex_ms = t0.elapsed_time(t1) / reps
+    del dbuf
 
     # ---- CG time to solution (even-odd preconditioned, D^dag D) -------------
     cg = None
@@ -374,7 +395,11 @@ def run_gpu(args, cfg):
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
                     "api": "lbcu_dphi_host (pinned host buffers, reference layout)",
-                    "check_rel_err": e2e_err},
+                    "check_rel_err": e2e_err,
+                    "pcie_bound": {"duplex_copy_ms_per_step": duplex_ms,
+                                   "frac": duplex_ms / (e2e_ms / e2e_steps),
+                                   "note": "concurrent pinned H2D + D2H of one step's bytes; "
+                                           "frac = that time / e2e ms per step"}},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cg": cg,
