@@ -12,7 +12,7 @@
  *   spinor       : [site][spin 4][colour dr] complex<double>   (2 doubles)
  *   gauge        : [site][mu 4][row dr][col dr] complex<double>, or double for
  *                  the adjoint representation (real_links)
- * Device storage is private to the library (even-odd, structure-of-arrays).
+ * Device storage is private to the library (even-odd, 32-site tiles).
  *
  * Status codes mirror the reference exception classes
  * (proj/include/latbench/errors.hpp:9-63): a non-zero return carries a
