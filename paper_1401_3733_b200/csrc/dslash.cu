@@ -206,13 +206,108 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
   }
 }
 
-template <int D, bool REAL, int FMT, bool BND, int EPI>
-__device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1]);
+// Both spin projections (1 -/+ g_mu) of the spinor at cb site nb from one load.
+template <int D, int P0, int P1, int F0, int F1>
+__device__ __forceinline__ void project2(double2 (&hm)[2][D], double2 (&hp)[2][D],
+                                         const double2* __restrict__ in, int nb, double s5) {
+  const double2* __restrict__ q = site_ptr<4 * D>(in, nb);
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const double2 a0 = ldg(q + (0 * D + c) * kTile);
+    const double2 a1 = ldg(q + (1 * D + c) * kTile);
+    const double2 b0 = phm<F0>(cscale(s5, ldg(q + (P0 * D + c) * kTile)));
+    const double2 b1 = phm<F1>(cscale(s5, ldg(q + (P1 * D + c) * kTile)));
+    hm[0][c] = cadd(a0, b0);
+    hm[1][c] = cadd(a1, b1);
+    hp[0][c] = csub(a0, b0);
+    hp[1][c] = csub(a1, b1);
+  }
+}
+
+// Colour frame of the accumulator: GF_AS4R works in the real basis Wt.
+template <int D, int FMT>
+__device__ __forceinline__ void to_frame(double2 (&h)[2][D]) {
+  if constexpr (FMT == GF_AS4R) {
+    double2 t[2][6];
+    as4r_in(t[0], h[0]);
+    as4r_in(t[1], h[1]);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < D; ++c) h[a][c] = t[a][c];
+  }
+}
+
+// g = M h in the accumulator frame, M = U or U^dag
+template <int D, bool REAL, int FMT, bool DAG>
+__device__ __forceinline__ void mul_frame(double2 (&g)[2][D], const ElemT<D, REAL, FMT>* p,
+                                          const double2 (&h)[2][D]) {
+  if constexpr (FMT == GF_AS4R) as4r_mul<DAG>(g, p, kTile, h);
+  else link_mul<D, REAL, FMT, DAG>(g, p, kTile, h);
+}
+
+template <int D>
+__device__ __forceinline__ double2 shfl_d2(unsigned mask, double2 v, int src) {
+  return make_double2(__shfl_sync(mask, v.x, src), __shfl_sync(mask, v.y, src));
+}
+
+// z hops with the neighbour spinors shared inside the warp (ZS kernels).
+// Needs every warp to cover whole z-rows of consecutive cb sites (Lz/2
+// divides 32, no site list): then both z-neighbours of an output site are
+// in[q] at its own cb index i (the "own" one: z+ when the site's z is even,
+// dz = 0; z- when odd) and at cb i -/+ 1 (row wrap i +/- (Lz/2 - 1)), which
+// is the own cb of another lane of the same row. Each lane loads only its
+// own in[q] spinor w and the two links stored at cb i (U_z^q(i), U_z^p(i)),
+// forms both projections and the backward product gb = U_z^q(i)^dag P+ w,
+// and hands its row neighbour what that lane is missing: gb (dz = 0 rows:
+// the consumer's backward hop) or P- w (dz = 1: the consumer's forward hop,
+// multiplied by the consumer's own U_z^p). Same arithmetic as hop_mu<3>, one
+// spinor load per site fewer.
+template <int D, bool REAL, int FMT>
+__device__ __forceinline__ void hop_z_shared(double2 (&acc)[4][D], const HopArgs& A,
+                                             const double2* __restrict__ in, int par, int i, int s,
+                                             unsigned mask) {
+  using G = Gam<3>;
+  const long long st = A.g.stride;
+  const int dz = s & 1;
+  const int hz = A.g.L[3] >> 1;  // cb sites per z-row
+  const int z = s % A.g.L[3];
+  int o;  // cb index of the other z-neighbour
+  if (dz == 0) o = (z == 0) ? i + hz - 1 : i - 1;
+  else o = (z == A.g.L[3] - 1) ? i - hz + 1 : i + 1;
+  const int src = (threadIdx.x & 31) + (o - i);
+  double2 hm[2][D], hp[2][D], gb[2][D];
+  project2<D, G::p0, G::p1, G::f0, G::f1>(hm, hp, in, i, A.s5in);
+  to_frame<D, FMT>(hm);
+  to_frame<D, FMT>(hp);
+  mul_frame<D, REAL, FMT, true>(gb, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, 3, i), hp);
+  double2 r[2][D];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) r[a][c] = shfl_d2<D>(mask, dz ? hm[a][c] : gb[a][c], src);
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double2 f = dz ? r[a][c] : hm[a][c];
+      const double2 b = dz ? gb[a][c] : r[a][c];
+      hm[a][c] = f;
+      gb[a][c] = b;
+    }
+  double2 gf[2][D];
+  mul_frame<D, REAL, FMT, false>(gf, link_ptr<D, REAL, FMT>(A.gauge, st, par, 3, i), hm);
+  reconstruct<D, G::r0, G::r1, G::q0, G::q1>(acc, gf);
+  reconstruct<D, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, gb);
+}
+
+template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS>
+__device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1], unsigned mask);
 template <int D, int EPI>
 __device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const double2 (&acc)[4][D],
                                          double (&nrm)[1]);
 
-template <int D, bool REAL, int FMT, bool BND, int EPI, int MINB>
+template <int D, bool REAL, int FMT, bool BND, int EPI, int MINB, bool ZS>
 __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ HopArgs A) {
   int par, blk;
   if (A.both) {
@@ -231,12 +326,17 @@ __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ 
     idx = blk * blockDim.x + threadIdx.x;
     ok = idx < A.nsites;
   }
-  if (ok) site_body<D, REAL, FMT, BND, EPI>(A, par, idx, nrm);
+  if constexpr (ZS) {
+    const unsigned mask = __ballot_sync(0xffffffffu, ok);
+    if (ok) site_body<D, REAL, FMT, BND, EPI, ZS>(A, par, idx, nrm, mask);
+  } else {
+    if (ok) site_body<D, REAL, FMT, BND, EPI, ZS>(A, par, idx, nrm, 0u);
+  }
   if constexpr (EPI != EPI_STORE) block_reduce_finalize<1>(A.red, nrm);
 }
 
-template <int D, bool REAL, int FMT, bool BND, int EPI>
-__device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1]) {
+template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS>
+__device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1], unsigned mask) {
   {
     const int i = A.list[par] ? A.list[par][idx] : idx;
     int c[4], s;
@@ -250,7 +350,8 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
     hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
     hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
     hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-    hop_mu<D, REAL, FMT, BND, 3>(acc, A, in, par, i, s, c);
+    if constexpr (ZS) hop_z_shared<D, REAL, FMT>(acc, A, in, par, i, s, mask);
+    else hop_mu<D, REAL, FMT, BND, 3>(acc, A, in, par, i, s, c);
     if constexpr (FMT == GF_AS4R) {  // back from the real-basis colour frame
 #pragma unroll
       for (int sp = 0; sp < 4; ++sp) as4r_out(acc[sp], 0.5);
@@ -400,44 +501,54 @@ int hop_block() {
 int hop_blocks(int nsites, int npar, int /*dr*/) { return (nsites + hop_block() - 1) / hop_block() * npar; }
 
 template <int D, bool REAL, int FMT, int MINB>
-void launch_hop_minb(const HopArgs& A, bool bnd, int epi, int blocks, cudaStream_t s) {
-#define LBCU_HOP_CASE(B, E)                                                         \
-  if (bnd == B && epi == E) {                                                       \
-    hop_kernel<D, REAL, FMT, B, E, MINB><<<blocks, hop_block(), 0, s>>>(A);         \
+void launch_hop_minb(const HopArgs& A, bool bnd, int epi, bool zs, int blocks, cudaStream_t s) {
+#define LBCU_HOP_CASE(B, E, Z)                                                      \
+  if (bnd == B && epi == E && zs == Z) {                                            \
+    hop_kernel<D, REAL, FMT, B, E, MINB, Z><<<blocks, hop_block(), 0, s>>>(A);      \
     return;                                                                         \
   }
-  LBCU_HOP_CASE(false, EPI_STORE)
-  LBCU_HOP_CASE(false, EPI_STORE_NORM)
-  LBCU_HOP_CASE(false, EPI_CG)
-  LBCU_HOP_CASE(true, EPI_STORE)
-  LBCU_HOP_CASE(true, EPI_STORE_NORM)
-  LBCU_HOP_CASE(true, EPI_CG)
+  if constexpr (D == 2 && !REAL) {
+    LBCU_HOP_CASE(false, EPI_STORE, true)
+    LBCU_HOP_CASE(false, EPI_STORE_NORM, true)
+    LBCU_HOP_CASE(false, EPI_CG, true)
+  }
+  LBCU_HOP_CASE(false, EPI_STORE, false)
+  LBCU_HOP_CASE(false, EPI_STORE_NORM, false)
+  LBCU_HOP_CASE(false, EPI_CG, false)
+  LBCU_HOP_CASE(true, EPI_STORE, false)
+  LBCU_HOP_CASE(true, EPI_STORE_NORM, false)
+  LBCU_HOP_CASE(true, EPI_CG, false)
 #undef LBCU_HOP_CASE
+  throw Error(LBCU_CONTRACT_VIOLATION, "hop: no kernel for this variant");
 }
 
 template <int D, bool REAL, int FMT>
 void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaStream_t s,
-                int blocks_override = 0) {
+                int blocks_override = 0, bool zs = false) {
   if (nsites <= 0) return;
+  // measured (profiles/r03_tune_zs_*, r03_tune_xcol_zs_*): +2.5 % for SU(2)
+  // fundamental; -1.5 % (SU(3) R12), -3 % (SU(2) adjoint), -15 % (AS4R) from
+  // the extra live values, so only the dr = 2 complex kernels share z hops
+  if constexpr (!(D == 2 && !REAL)) zs = false;
   const int blocks = blocks_override > 0 ? blocks_override : hop_blocks(nsites, npar, D);
   if constexpr (D <= 3) {
     const int minb = env_int("LBCU_HOP_MINB", default_minb<D, REAL, FMT>());
     if (minb == 4) {
-      launch_hop_minb<D, REAL, FMT, 4>(A, bnd, epi, blocks, s);
+      launch_hop_minb<D, REAL, FMT, 4>(A, bnd, epi, zs, blocks, s);
       return;
     }
     if constexpr (D == 2 && FMT == GF_SU2) {
       if (minb == 5) {
-        launch_hop_minb<D, REAL, FMT, 5>(A, bnd, epi, blocks, s);
+        launch_hop_minb<D, REAL, FMT, 5>(A, bnd, epi, zs, blocks, s);
         return;
       }
     }
     if (minb == 3) {
-      launch_hop_minb<D, REAL, FMT, 3>(A, bnd, epi, blocks, s);
+      launch_hop_minb<D, REAL, FMT, 3>(A, bnd, epi, zs, blocks, s);
       return;
     }
   }
-  launch_hop_minb<D, REAL, FMT, 1>(A, bnd, epi, blocks, s);
+  launch_hop_minb<D, REAL, FMT, 1>(A, bnd, epi, zs, blocks, s);
 }
 
 // Supported representation dimensions and storage formats (compile-time
@@ -557,8 +668,11 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       A.red = Reduce{ctx->partials, ctx->ticket, c.result, 0, blocks,
                      c.post, ctx->dcg, ctx->dhist, c.handle, c.use_graph};
     }
+    // warp-shared z hops when every warp covers whole z-rows (hop_z_shared)
+    const int hz = geo.local[3] / 2;
+    const bool zs = env_int("LBCU_HOP_ZS", 1) && hz > 0 && 32 % hz == 0;
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s, blocks);
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s, blocks, zs);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaGetLastError());
