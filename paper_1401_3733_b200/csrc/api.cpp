@@ -312,10 +312,11 @@ int lbcu_ctx_destroy(lbcu_ctx c) {
   host_pipe_release(c);
   for (auto& kv : c->scratch) free_spinor(kv.second);
   for (auto& kv : c->halo)
-    for (int f = 0; f < 8; ++f) {
-      if (kv.second.send[f]) cudaFree(kv.second.send[f]);
-      if (kv.second.recv[f]) cudaFree(kv.second.recv[f]);
-    }
+    for (int p = 0; p < 2; ++p)
+      for (int f = 0; f < 8; ++f) {
+        if (kv.second.send[p][f]) cudaFree(kv.second.send[p][f]);
+        if (kv.second.recv[p][f]) cudaFree(kv.second.recv[p][f]);
+      }
   for (int p = 0; p < 2; ++p) {
     if (c->ilist[p]) cudaFree(c->ilist[p]);
     if (c->blist[p]) cudaFree(c->blist[p]);

@@ -47,8 +47,8 @@ struct HopArgs {
   int both;    // 1: parity = blockIdx.x & 1
   int nsites;  // sites per parity
   const int* list[2];
-  const double2* hfwd[4];
-  const double2* hbwd[4];
+  const double2* hfwd[2][4];  // halos by output parity and mu (boundary launches)
+  const double2* hbwd[2][4];
   int hcount[4];
   // antiperiodic time sign applied in-kernel (compact formats): the U_0 link
   // whose global time coordinate is bc_tlast carries a factor -1
@@ -167,7 +167,7 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int cc = 0; cc < D; ++cc) h[a][cc] = ldg(A.hfwd[MU] + (a * D + cc) * hc + j);
+        for (int cc = 0; cc < D; ++cc) h[a][cc] = ldg(A.hfwd[par][MU] + (a * D + cc) * hc + j);
     } else {
       project<D, G::p0, G::p1, G::f0, G::f1>(h, in, st, nb_fwd(A.g, s, c, MU) >> 1, A.s5in);
     }
@@ -183,7 +183,7 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int cc = 0; cc < D; ++cc) g[a][cc] = ldg(A.hbwd[MU] + (a * D + cc) * hc + j);
+        for (int cc = 0; cc < D; ++cc) g[a][cc] = ldg(A.hbwd[par][MU] + (a * D + cc) * hc + j);
       if constexpr (FMT == GF_AS4R) {  // halo records are in the standard basis
         double2 t[2][D];
         as4r_in(t[0], g[0]);
@@ -457,15 +457,27 @@ __device__ __forceinline__ void pack_site(const PackArgs& P, int j) {
   }
 }
 
+// All faces of all requested parities in one launch: job k covers blocks
+// [first[k], first[k + 1]) and packs one (parity, face) record set.
+constexpr int kMaxPackJobs = 16;
+struct PackAll {
+  PackArgs job[kMaxPackJobs];
+  int first[kMaxPackJobs + 1];
+  int njobs;
+};
+
 template <int D, bool REAL, int FMT>
-__global__ void __launch_bounds__(128) pack_kernel(const __grid_constant__ PackArgs P) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= P.count) return;
-  switch (P.mu) {
-    case 0: pack_site<D, REAL, FMT, 0>(P, j); break;
-    case 1: pack_site<D, REAL, FMT, 1>(P, j); break;
-    case 2: pack_site<D, REAL, FMT, 2>(P, j); break;
-    default: pack_site<D, REAL, FMT, 3>(P, j); break;
+__global__ void __launch_bounds__(128) pack_kernel(const __grid_constant__ PackAll P) {
+  int k = 0;
+  while (k + 1 < P.njobs && (int)blockIdx.x >= P.first[k + 1]) ++k;
+  const PackArgs& J = P.job[k];
+  const int j = (blockIdx.x - P.first[k]) * blockDim.x + threadIdx.x;
+  if (j >= J.count) return;
+  switch (J.mu) {
+    case 0: pack_site<D, REAL, FMT, 0>(J, j); break;
+    case 1: pack_site<D, REAL, FMT, 1>(J, j); break;
+    case 2: pack_site<D, REAL, FMT, 2>(J, j); break;
+    default: pack_site<D, REAL, FMT, 3>(P.job[k], j); break;
   }
 }
 
@@ -591,14 +603,15 @@ HaloBufs& halo_bufs(lbcu_ctx_s* ctx, int dr) {
   size_t need = 0;
   for (int f = 0; f < 8; ++f) need = std::max<size_t>(need, 2 * dr * ctx->plan.count[f]);
   if (hb.cap < need) {
-    for (int f = 0; f < 8; ++f) {
-      if (hb.send[f]) cudaFree(hb.send[f]);
-      if (hb.recv[f]) cudaFree(hb.recv[f]);
-      hb.send[f] = hb.recv[f] = nullptr;
-      if (ctx->plan.count[f] == 0) continue;
-      LBCU_CUDA(cudaMalloc(&hb.send[f], need * sizeof(double2)));
-      LBCU_CUDA(cudaMalloc(&hb.recv[f], need * sizeof(double2)));
-    }
+    for (int p = 0; p < 2; ++p)
+      for (int f = 0; f < 8; ++f) {
+        if (hb.send[p][f]) cudaFree(hb.send[p][f]);
+        if (hb.recv[p][f]) cudaFree(hb.recv[p][f]);
+        hb.send[p][f] = hb.recv[p][f] = nullptr;
+        if (ctx->plan.count[f] == 0) continue;
+        LBCU_CUDA(cudaMalloc(&hb.send[p][f], need * sizeof(double2)));
+        LBCU_CUDA(cudaMalloc(&hb.recv[p][f], need * sizeof(double2)));
+      }
     hb.cap = need;
   }
   return hb;
@@ -680,25 +693,21 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   }
 
   // ---- decomposed: pack -> exchange -> interior -> boundary -------------
+  // One fused pack launch for every (output parity, face), one exchange, then
+  // one interior and one boundary launch covering the requested parities
+  // (per parity only if their site counts differ).
   HaloBufs& hb = halo_bufs(ctx, dr);
-  int total_blocks = 0, int_blocks[2] = {0, 0}, bnd_blocks[2] = {0, 0};
-  for (int k = 0; k < npar; ++k) {
-    const int p = pars[k];
-    int_blocks[k] = hop_blocks(ctx->nint[p], 1, dr);
-    bnd_blocks[k] = hop_blocks(ctx->nbnd[p], 1, dr);
-    total_blocks += int_blocks[k] + bnd_blocks[k];
-  }
-  if (reduce && total_blocks > ctx->max_partials)
-    throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
   if (c.post != POST_NONE)
     throw Error(LBCU_CONTRACT_VIOLATION, "fused CG scalar steps need a single rank");
-  // one exchange per output parity keeps the message buffers simple
+  PackAll PA{};
+  std::vector<Transport::Msg> msgs;
+  int pack_blocks = 0;
   for (int k = 0; k < npar; ++k) {
     const int p = pars[k], q = p ^ 1;
-    std::vector<Transport::Msg> msgs;
     for (int f = 0; f < 8; ++f) {
       if (ctx->plan.count[f] == 0) continue;
-      PackArgs P{};
+      if (PA.njobs == kMaxPackJobs) throw Error(LBCU_CUDA_ERROR, "too many halo faces");
+      PackArgs& P = PA.job[PA.njobs];
       P.g = ctx->dgeo;
       P.in = c.in->par[q];
       P.gauge = c.g->base;
@@ -710,58 +719,83 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       P.bc_kernel = A.bc_kernel;
       P.t_off = A.t_off;
       P.bc_tlast = A.bc_tlast;
-      P.outbuf = hb.send[f];
-      dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-        pack_kernel<LBCU_TPARAMS(Dc, Rc, Fc)><<<(P.count + kBlock - 1) / kBlock, kBlock, 0, s>>>(P);
-      });
-      ctx->launches += 1;
+      P.outbuf = hb.send[p][f];
+      PA.first[PA.njobs] = pack_blocks;
+      pack_blocks += (P.count + kBlock - 1) / kBlock;
+      PA.njobs++;
       // face f goes to partner[f]; the matching halo arrives from the opposite
       // partner into recv[f ^ 1] (dir 0 record -> receiver's forward halo)
       Transport::Msg m;
-      m.send = hb.send[f];
-      m.recv = hb.recv[f ^ 1];
+      m.send = hb.send[p][f];
+      m.recv = hb.recv[p][f ^ 1];
       m.bytes = sizeof(double2) * 2 * dr * ctx->plan.count[f];
       m.peer_send = ctx->plan.partner[f];
       m.peer_recv = ctx->plan.partner[f ^ 1];
       msgs.push_back(m);
     }
-    LBCU_CUDA(cudaGetLastError());
-    // interior sites (no halo dependency) run on the compute stream while the
-    // halos travel on the comm stream; boundary sites wait for both.
-    HopArgs Ai = A;
-    Ai.both = 0;
-    Ai.par0 = p;
-    Ai.nsites = ctx->nint[p];
-    Ai.list[p] = ctx->ilist[p];
-    int off = 0;
-    for (int kk = 0; kk < k; ++kk) off += int_blocks[kk] + bnd_blocks[kk];
-    if (reduce) Ai.red = Reduce{ctx->partials, ctx->ticket, c.result, off, total_blocks};
-    LBCU_CUDA(cudaEventRecord(ctx->ev_pack, s));
+  }
+  PA.first[PA.njobs] = pack_blocks;
+  if (pack_blocks > 0) {
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ai, false, c.epi, Ai.nsites, 1, s);
-    });
-    ctx->launches += 1;
-    LBCU_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_pack, 0));
-    ctx->world->t->exchange(ctx->rank, msgs, ctx->comm_stream);
-    LBCU_CUDA(cudaEventRecord(ctx->ev_comm, ctx->comm_stream));
-    LBCU_CUDA(cudaStreamWaitEvent(s, ctx->ev_comm, 0));
-    HopArgs Ab = Ai;
-    Ab.nsites = ctx->nbnd[p];
-    Ab.list[p] = ctx->blist[p];
-    for (int mu = 0; mu < 4; ++mu) {
-      // recv[2 mu + 1] holds the +mu partner's dir-0 face (forward halo),
-      // recv[2 mu] the -mu partner's dir-1 face (backward halo)
-      Ab.hfwd[mu] = hb.recv[2 * mu + 1];
-      Ab.hbwd[mu] = hb.recv[2 * mu + 0];
-      Ab.hcount[mu] = static_cast<int>(ctx->plan.count[2 * mu]);
-    }
-    if (reduce) Ab.red = Reduce{ctx->partials, ctx->ticket, c.result, off + int_blocks[k], total_blocks};
-    dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ab, true, c.epi, Ab.nsites, 1, s);
+      pack_kernel<LBCU_TPARAMS(Dc, Rc, Fc)><<<pack_blocks, kBlock, 0, s>>>(PA);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaGetLastError());
   }
+  // launch groups: both parities in one launch when their site counts agree
+  const bool joint = npar == 2 && ctx->nint[0] == ctx->nint[1] && ctx->nbnd[0] == ctx->nbnd[1];
+  const int ngroups = joint ? 1 : npar;
+  int int_blocks[2] = {0, 0}, bnd_blocks[2] = {0, 0}, total_blocks = 0;
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const int p = pars[gi], np = joint ? 2 : 1;
+    int_blocks[gi] = hop_blocks(ctx->nint[p], np, dr);
+    bnd_blocks[gi] = hop_blocks(ctx->nbnd[p], np, dr);
+    total_blocks += int_blocks[gi] + bnd_blocks[gi];
+  }
+  if (reduce && total_blocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
+  auto group_args = [&](int gi, bool bnd) {
+    HopArgs G = A;
+    const int p = pars[gi];
+    G.both = joint ? 1 : 0;
+    G.par0 = p;
+    G.nsites = bnd ? ctx->nbnd[p] : ctx->nint[p];
+    for (int pp = 0; pp < 2; ++pp) G.list[pp] = bnd ? ctx->blist[pp] : ctx->ilist[pp];
+    int off = 0;
+    for (int g2 = 0; g2 < gi; ++g2) off += int_blocks[g2] + bnd_blocks[g2];
+    if (bnd) off += int_blocks[gi];
+    if (reduce) G.red = Reduce{ctx->partials, ctx->ticket, c.result, off, total_blocks};
+    return G;
+  };
+  // interior sites (no halo dependency) run on the compute stream while the
+  // halos travel on the comm stream; boundary sites wait for both.
+  LBCU_CUDA(cudaEventRecord(ctx->ev_pack, s));
+  for (int gi = 0; gi < ngroups; ++gi) {
+    HopArgs Ai = group_args(gi, false);
+    dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ai, false, c.epi, Ai.nsites, joint ? 2 : 1, s);
+    });
+    ctx->launches += 1;
+  }
+  LBCU_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_pack, 0));
+  ctx->world->t->exchange(ctx->rank, msgs, ctx->comm_stream);
+  LBCU_CUDA(cudaEventRecord(ctx->ev_comm, ctx->comm_stream));
+  LBCU_CUDA(cudaStreamWaitEvent(s, ctx->ev_comm, 0));
+  for (int gi = 0; gi < ngroups; ++gi) {
+    HopArgs Ab = group_args(gi, true);
+    for (int pp = 0; pp < 2; ++pp)
+      for (int mu = 0; mu < 4; ++mu) {
+        // recv[2 mu + 1] holds the +mu partner's dir-0 face (forward halo),
+        // recv[2 mu] the -mu partner's dir-1 face (backward halo)
+        Ab.hfwd[pp][mu] = hb.recv[pp][2 * mu + 1];
+        Ab.hbwd[pp][mu] = hb.recv[pp][2 * mu + 0];
+        Ab.hcount[mu] = static_cast<int>(ctx->plan.count[2 * mu]);
+      }
+    dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ab, true, c.epi, Ab.nsites, joint ? 2 : 1, s);
+    });
+    ctx->launches += 1;
+  }
+  LBCU_CUDA(cudaGetLastError());
 }
 
 }  // namespace lbcu

@@ -39,8 +39,8 @@ namespace lbcu {
 enum Epi { EPI_STORE = 0, EPI_STORE_NORM = 1, EPI_CG = 2 };
 
 struct HaloBufs {
-  double2* send[8] = {};
-  double2* recv[8] = {};
+  double2* send[2][8] = {};  // by output parity, face
+  double2* recv[2][8] = {};
   size_t cap = 0;  // double2 per buffer
 };
 
