@@ -272,7 +272,7 @@ int lbcu_ctx_create(lbcu_world w, int rank, int device, const int global[4], con
   LBCU_CUDA(cudaMemset(ctx->dscal, 0, sizeof(double) * 64));
   LBCU_CUDA(cudaMallocHost(&ctx->hscal, sizeof(double) * 64));
   LBCU_CUDA(cudaMalloc(&ctx->dcg, sizeof(CgState)));
-  LBCU_CUDA(cudaMallocHost(&ctx->hcg, sizeof(CgState)));
+  LBCU_CUDA(cudaMallocHost(&ctx->hcg, 3 * sizeof(CgState)));  // [0] final, [1..2] per-iteration ring
 
   if (g.any_decomposed) {  // interior / boundary site lists per parity
     for (int p = 0; p < 2; ++p) {
@@ -331,6 +331,8 @@ int lbcu_ctx_destroy(lbcu_ctx c) {
   if (c->staging) cudaFree(c->staging);
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaEventDestroy(c->ev_pack);
+  for (int e = 0; e < 2; ++e)
+    if (c->ev_cg[e]) cudaEventDestroy(c->ev_cg[e]);
   cudaEventDestroy(c->ev_comm);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->comm_stream);

@@ -79,6 +79,7 @@ __global__ void k_gamma5(double2* __restrict__ f, size_t block_elems, size_t hal
 // x += alpha p_old ; p = r + beta p_old      (deferred x update)
 __global__ void k_cg_p(double2* __restrict__ p, const double2* __restrict__ r, double2* __restrict__ x,
                        size_t n, const CgState* __restrict__ st) {
+  if (st->done) return;  // speculative iteration after convergence (device.cuh)
   const double alpha = st->alpha, beta = st->beta;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const double2 pv = p[i], rv = __ldg(r + i);
@@ -134,10 +135,7 @@ __global__ void k_cg_init(CgState* st, const double* b2, double tol, long long m
   st->done = 0;
 }
 
-__global__ void k_cg_alpha(CgState* st, const double* pap) {
-  st->pap = *pap;
-  st->alpha = st->rr / st->pap;
-}
+__global__ void k_cg_alpha(CgState* st, const double* pap) { cg_post_alpha(st, *pap); }
 
 // end of iteration k (solver.cpp:58-69): relative residual, history,
 // convergence, beta, rr <- rr_new; optionally drives a graph while-loop.

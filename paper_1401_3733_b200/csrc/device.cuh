@@ -138,13 +138,18 @@ struct CgState {
 // CG scalar steps (solver.cpp:53-69), run by one thread: either a 1-thread
 // kernel after a multi-rank allreduce, or fused into the last block of the
 // reduction that produced the value (single rank).
+// Every CG state step is a no-op once the solve is done: the multi-rank host
+// loop enqueues iteration k + 1 before it has read iteration k's state, and
+// that speculative iteration must leave x, p and the state untouched.
 __device__ __forceinline__ void cg_post_alpha(CgState* st, double pap) {
+  if (st->done) return;
   st->pap = pap;
   st->alpha = st->rr / pap;
 }
 
 __device__ __forceinline__ void cg_post_end(CgState* st, double rrn, double* hist,
                                             unsigned long long handle, int use_graph) {
+  if (st->done) return;
   const double rel = sqrt(rrn) / st->bnorm;
   const long long k = st->k;
   hist[k] = rel;

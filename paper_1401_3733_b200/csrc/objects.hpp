@@ -70,12 +70,13 @@ struct lbcu_ctx_s {
   std::map<int, lbcu::HaloBufs> halo;  // keyed by dr
   std::map<std::tuple<int, int, int>, lbcu_spinor_s*> scratch;  // (dr, subset, slot)
   lbcu::CgState* dcg = nullptr;
-  lbcu::CgState* hcg = nullptr;  // pinned
+  lbcu::CgState* hcg = nullptr;  // pinned, 3: final state + 2-slot per-iteration ring
   double* dhist = nullptr;
   long long hist_cap = 0;
   void* staging = nullptr;  // device staging buffer for host<->device layout transposes
   size_t staging_bytes = 0;
   long long launches = 0;
+  cudaEvent_t ev_cg[2] = {nullptr, nullptr};  // per-iteration CG state copies (host loop)
   // host-field pipeline (lbcu_dphi_host): 2 slots, copy-in / copy-out streams
   struct HostPipe {
     size_t bytes = 0;

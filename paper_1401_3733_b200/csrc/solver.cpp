@@ -295,12 +295,27 @@ int run_cg(lbcu_ctx_s* ctx, const lbcu_cg_settings* st, lbcu_spinor_s* rhs, lbcu
     LBCU_CUDA(cudaMemcpyAsync(ctx->hcg, ctx->dcg, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
     LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->launches += ge->body_kernels * ctx->hcg->k;
-  } else {
+  } else if (fused) {
+    // host loop one iteration ahead: iteration k + 1 is enqueued before the
+    // state of iteration k is read back, so the device never idles on the
+    // host round trip; a speculative iteration after convergence is a no-op
+    // on x, p and the state (device.cuh: cg_post_*; blas.cu: k_cg_p)
+    for (int e = 0; e < 2; ++e)
+      if (!ctx->ev_cg[e]) LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_cg[e], cudaEventDisableTiming));
     for (int k = 0; k < st->max_iterations; ++k) {
-      if (fused)
-        fused_body(ctx, *fused, x, r, p, q, t, 0, 0);
-      else
-        callback_body(ctx, op, user, x, r, p, q);
+      fused_body(ctx, *fused, x, r, p, q, t, 0, 0);
+      CgState* h = ctx->hcg + 1 + (k & 1);
+      LBCU_CUDA(cudaMemcpyAsync(h, ctx->dcg, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
+      LBCU_CUDA(cudaEventRecord(ctx->ev_cg[k & 1], ctx->stream));
+      if (k == 0) continue;
+      LBCU_CUDA(cudaEventSynchronize(ctx->ev_cg[(k - 1) & 1]));
+      if (ctx->hcg[1 + ((k - 1) & 1)].done) break;
+    }
+    LBCU_CUDA(cudaMemcpyAsync(ctx->hcg, ctx->dcg, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
+    LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
+    for (int k = 0; k < st->max_iterations; ++k) {  // the callback runs exactly once per iteration
+      callback_body(ctx, op, user, x, r, p, q);
       LBCU_CUDA(cudaMemcpyAsync(ctx->hcg, ctx->dcg, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
       LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
       if (ctx->hcg->done) break;

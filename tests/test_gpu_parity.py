@@ -318,3 +318,27 @@ def test_non_group_links_stay_dense():
     inp, out = lb.SpinorField(ctx, 3).upload(s), lb.SpinorField(ctx, 3)
     lb.apply_dirac(out, gauge, inp, 0.1)
     assert rel_l2(out.download(), O.port_dirac(L, 1, 0.1, g, s)) < TOL_DPHI
+
+
+@pytest.mark.parametrize("solver", ["eo", "h"])
+def test_cg_host_loop_matches_graph(solver, monkeypatch):
+    """The host-driven loop (multi-rank path, one iteration enqueued ahead of
+    the state read-back) gives the same iterations, history and solution as
+    the single-rank CUDA-graph loop: the speculative iteration after
+    convergence must leave x, p and the CG state untouched."""
+    L = [8, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, 2, lb.FUNDAMENTAL)
+    sub = lb.EVEN if solver == "eo" else lb.FULL
+    rhs = lb.SpinorField(ctx, dr, sub).upload(s)
+    st = lb.CgSettings(1e-10, 1000)
+    run = lb.cg_solve_eo if solver == "eo" else lb.cg_solve_h
+    a = run(gauge, 0.1, rhs, st)
+    monkeypatch.setenv("LBCU_CG_GRAPH", "0")
+    b = run(gauge, 0.1, rhs, st)
+    assert a.iterations == b.iterations
+    assert np.array_equal(np.asarray(a.residual_history), np.asarray(b.residual_history))
+    assert np.array_equal(a.solution.download(), b.solution.download())
+    assert a.true_rel_residual == b.true_rel_residual
+    # a tolerance reached at the iteration cap: the loop stops at max_iterations
+    with pytest.raises(lb.NonConvergence):
+        run(gauge, 0.1, rhs, lb.CgSettings(1e-10, a.iterations - 2))
