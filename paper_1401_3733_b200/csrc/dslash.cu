@@ -159,7 +159,7 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
                                        const int c[4]) {
   using G = Gam<MU>;
   const long long st = A.g.stride;
-  {  // forward: (1 - g_mu) U_mu(x) in(x + mu)
+  auto fwd = [&] {  // forward: (1 - g_mu) U_mu(x) in(x + mu)
     double2 h[2][D];
     if (BND && !A.g.wrap[MU] && c[MU] == A.g.L[MU] - 1) {
       const int j = face_pos(A.g, c, MU) >> 1;
@@ -174,8 +174,8 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
     if constexpr (MU == 0) bc_sign<D, FMT>(h, A.bc_kernel && A.t_off + c[0] == A.bc_tlast);
     link_hop<D, REAL, FMT, false, G::r0, G::r1, G::q0, G::q1>(
         acc, link_ptr<D, REAL, FMT>(A.gauge, st, par, MU, i), st, h);
-  }
-  {  // backward: (1 + g_mu) U_mu(x - mu)^dag in(x - mu)
+  };
+  auto bwd = [&] {  // backward: (1 + g_mu) U_mu(x - mu)^dag in(x - mu)
     if (BND && !A.g.wrap[MU] && c[MU] == 0) {
       double2 g[2][D];
       const int j = face_pos(A.g, c, MU) >> 1;
@@ -203,6 +203,16 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
       link_hop<D, REAL, FMT, true, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(
           acc, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, MU, nb), st, h);
     }
+  };
+#ifndef LBCU_HOP_BWDFIRST
+#define LBCU_HOP_BWDFIRST 0
+#endif
+  if constexpr (LBCU_HOP_BWDFIRST) {
+    bwd();
+    fwd();
+  } else {
+    fwd();
+    bwd();
   }
 }
 
@@ -347,11 +357,54 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
 #pragma unroll
       for (int cc = 0; cc < D; ++cc) acc[k][cc] = make_double2(0.0, 0.0);
     const double2* in = A.in[par ^ 1];
-    hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
-    hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
-    hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-    if constexpr (ZS) hop_z_shared<D, REAL, FMT>(acc, A, in, par, i, s, mask);
-    else hop_mu<D, REAL, FMT, BND, 3>(acc, A, in, par, i, s, c);
+    // Direction order (profiles/r03_tune_order*): z y x t is 6 % faster for
+    // the full Dphi and 2-5 % for the eo hop with SU(2) links (fundamental and
+    // adjoint); t x y z stays best for R12 and AS4R. -DLBCU_HOP_ORDER=k
+    // forces one order for A/B builds (tools/build_variant.sh).
+#ifndef LBCU_HOP_ORDER
+#define LBCU_HOP_ORDER -1
+#endif
+    constexpr int kOrder = LBCU_HOP_ORDER >= 0 ? LBCU_HOP_ORDER : (FMT == GF_SU2 || (D == 2 && !REAL)) ? 1 : 0;
+    auto z_hop = [&] {
+      if constexpr (ZS) hop_z_shared<D, REAL, FMT>(acc, A, in, par, i, s, mask);
+      else hop_mu<D, REAL, FMT, BND, 3>(acc, A, in, par, i, s, c);
+    };
+    if constexpr (kOrder == 1) {  // z y x t
+      z_hop();
+      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
+    } else if constexpr (kOrder == 5) {  // y z x t
+      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
+      z_hop();
+      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
+    } else if constexpr (kOrder == 6) {  // z y t x
+      z_hop();
+      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
+    } else if constexpr (kOrder == 7) {  // z x y t
+      z_hop();
+      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
+    } else if constexpr (kOrder == 2) {  // t z x y
+      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
+      z_hop();
+      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
+    } else if constexpr (kOrder == 3) {  // x t y z
+      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
+      z_hop();
+    } else {  // t x y z
+      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
+      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
+      z_hop();
+    }
     if constexpr (FMT == GF_AS4R) {  // back from the real-basis colour frame
 #pragma unroll
       for (int sp = 0; sp < 4; ++sp) as4r_out(acc[sp], 0.5);
