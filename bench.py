@@ -10,8 +10,11 @@ config the metric is quoted on at N = 1). A step is one full Dphi
 application over the lattice, inputs resident in HBM. One JSON line on rank 0.
 
 Under torchrun (N > 1) each rank owns one GPU and one sub-lattice (T split
-first, then Z: SURVEY.md §8e); halos move through the library's NCCL
-transport; time is the max over ranks of CUDA-event time.
+first, then Z: SURVEY.md §8e). Halos go straight from the pack kernel into
+the neighbour's receive arena over NVLink (the library's IPC world), checked
+once per run bit for bit against NCCL send/recv halos (LBCU_TRANSPORT=nccl
+forces NCCL); CG sums use NCCL. Time is the max over ranks of CUDA-event
+time.
 
 --impl reference times the reference's own CPU apply_dirac (oracle/_ref, the
 unmodified latbench compiled from its sources) with all host threads on the
@@ -249,9 +252,22 @@ def run_gpu(args, cfg):
 
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        obj = [lb.World.nccl_unique_id() if rank == 0 else None]
+        import uuid
+        obj = [(lb.World.nccl_unique_id(), f"/lbcu_{uuid.uuid4().hex[:16]}") if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        world = lb.World.nccl(ws, rank, obj[0])
+        uid, shm_name = obj[0]
+        # halos: direct peer-memory stores by the pack kernel (IPC world; NCCL
+        # for the CG sums), checked below against NCCL send/recv halos;
+        # LBCU_TRANSPORT=nccl forces the NCCL world
+        transport = os.environ.get("LBCU_TRANSPORT", "ipc")
+        world = None
+        if transport == "ipc":
+            try:
+                world = lb.World.ipc(ws, rank, shm_name, uid)
+            except Exception as e:  # noqa: BLE001
+                transport = f"nccl (ipc world unavailable: {e})"
+        if world is None:
+            world = lb.World.nccl(ws, rank, uid)
     dr = lb.rep_dim(rep, n)
     real = lb.rep_is_real(rep)
     links = {"haar": lb.LINKS_HAAR, "near_unit": lb.LINKS_NEAR_UNIT}[cfg["links"]]
@@ -270,6 +286,22 @@ def run_gpu(args, cfg):
     fmt, fmt_err = gauge.storage()
     a = lb.SpinorField(ctx, dr).upload(s)
     b = lb.SpinorField(ctx, dr)
+    if ws > 1 and transport == "ipc":
+        # the direct halos must reproduce the NCCL send/recv halos bit for bit
+        lb.apply_dirac(b, gauge, a, mass)
+        world.set_direct(False)
+        c2 = lb.SpinorField(ctx, dr)
+        lb.apply_dirac(c2, gauge, a, mass)
+        lb.axpy(c2, -1.0, b)
+        diff = lb.sqnorm(c2)
+        del c2
+        if diff == 0.0:
+            world.set_direct(True)
+            transport = "ipc (direct peer-memory halos, checked bit-identical to NCCL send/recv)"
+        else:
+            transport = f"nccl (ipc halos differed from NCCL: |diff|^2 = {diff:.3e})"
+    elif ws > 1:
+        transport = transport if transport != "ipc" else "nccl"
 
     def barrier():
         ctx.synchronize()
@@ -392,6 +424,7 @@ def run_gpu(args, cfg):
             "config": {"workload": cfg["name"], "lattice_TXYZ": L, "group_rank": n, "rep": rep, "dr": dr,
                        "mass": mass, "bc": "periodic space, antiperiodic time", "grid": grid,
                        "parallelism": f"domain decomposition {grid}",
+                       "halo_transport": transport if ws > 1 else "none (one rank)",
                        "l2": f"inputs larger than L2 ({(bpsite * V) / 1e6:.0f} MB touched per step vs 126 MB)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,

@@ -113,6 +113,21 @@ int lbcu_world_threads(int nranks, lbcu_world* out);
  * lbcu_nccl_unique_id on rank 0, broadcast out of band. */
 int lbcu_nccl_unique_id(unsigned char id[128]);
 int lbcu_world_nccl(int nranks, int rank, const unsigned char id[128], lbcu_world* out);
+/* One process per GPU on one node with direct halos (replaces the same
+ * halo_exchange, transport.cpp:142-221): the halo pack kernel stores its
+ * records straight into the receiving rank's arena over NVLink (CUDA IPC
+ * mappings); completion is an interprocess event per exchange, recorded after
+ * the pack and waited on by the peer's stream before its boundary kernel, with
+ * a host barrier in the POSIX shared-memory segment `name` ("/...", unique per
+ * job) between the two. No kernel waits on another rank. nccl_id (nullable):
+ * CG sums through NCCL; NULL sums through the segment on the host. */
+int lbcu_world_ipc(int nranks, int rank, const char* name, const unsigned char* nccl_id, lbcu_world* out);
+/* The thread world with the same direct halo protocol (test and emulation). */
+int lbcu_world_threads_direct(int nranks, lbcu_world* out);
+/* Collective: direct halos on (1) or message exchange (0; the IPC world then
+ * sends the halos through its NCCL communicator). Worlds without a direct
+ * mode accept only 0. */
+int lbcu_world_set_direct(lbcu_world w, int on);
 int lbcu_world_destroy(lbcu_world w);
 
 /* ---- contexts: build_geometry + build_exchange_plan + Worker ------------- */

@@ -127,6 +127,9 @@ def lib():
             "lbcu_plan_faces": (C.c_int, [_ip, _ip, C.c_int, C.c_int, _ip, _ip, C.POINTER(C.c_int32)]),
             "lbcu_world_single": (C.c_int, [C.POINTER(_vp)]),
             "lbcu_world_threads": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+            "lbcu_world_threads_direct": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+            "lbcu_world_set_direct": (C.c_int, [_vp, C.c_int]),
+            "lbcu_world_ipc": (C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.POINTER(_vp)]),
             "lbcu_nccl_unique_id": (C.c_int, [C.c_char_p]),
             "lbcu_world_nccl": (C.c_int, [C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
             "lbcu_world_destroy": (C.c_int, [_vp]),
@@ -282,10 +285,23 @@ class World:
         return cls(h)
 
     @classmethod
-    def threads(cls, nranks: int):
-        """In-process world: one host thread per rank (reference run_workers)."""
+    def threads(cls, nranks: int, direct: bool = False):
+        """In-process world: one host thread per rank (reference run_workers).
+        direct: halos stored by the pack kernel into the peer's arena (the IPC
+        world's protocol) instead of copied between barriers."""
         h = _vp()
-        _check(lib().lbcu_world_threads(int(nranks), C.byref(h)))
+        fn = lib().lbcu_world_threads_direct if direct else lib().lbcu_world_threads
+        _check(fn(int(nranks), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def ipc(cls, nranks: int, rank: int, name: str, uid: Optional[bytes] = None):
+        """One process per GPU on one node, direct peer-memory halos (CUDA IPC);
+        `name`: a POSIX shared-memory name ("/...") unique to the job; `uid`:
+        an NCCL unique id for the CG sums (None: sums through the segment)."""
+        h = _vp()
+        _check(lib().lbcu_world_ipc(int(nranks), int(rank), name.encode(),
+                                    None if uid is None else C.c_char_p(uid), C.byref(h)))
         return cls(h)
 
     @staticmethod
@@ -299,6 +315,10 @@ class World:
         h = _vp()
         _check(lib().lbcu_world_nccl(int(nranks), int(rank), C.c_char_p(uid), C.byref(h)))
         return cls(h)
+
+    def set_direct(self, on: bool):
+        """Collective: direct peer-memory halos (True) or message exchange."""
+        _check(lib().lbcu_world_set_direct(self._h, 1 if on else 0))
 
     def close(self):
         if self._h:

@@ -197,6 +197,35 @@ int lbcu_world_threads(int nranks, lbcu_world* out) {
   API_END
 }
 
+int lbcu_world_threads_direct(int nranks, lbcu_world* out) {
+  API_BEGIN
+  auto* w = new lbcu_world_s;
+  w->t = make_thread_transport(nranks, true);
+  *out = w;
+  API_END
+}
+
+int lbcu_world_ipc(int nranks, int rank, const char* name, const unsigned char* nccl_id, lbcu_world* out) {
+  API_BEGIN
+  need(out != nullptr, "lbcu_world_ipc: null output");
+  auto* w = new lbcu_world_s;
+  try {
+    w->t = make_ipc_transport(nranks, rank, name, nccl_id);
+  } catch (...) {
+    delete w;
+    throw;
+  }
+  *out = w;
+  API_END
+}
+
+int lbcu_world_set_direct(lbcu_world w, int on) {
+  API_BEGIN
+  need(w != nullptr, "lbcu_world_set_direct: null world");
+  w->t->set_direct(on != 0);
+  API_END
+}
+
 int lbcu_nccl_unique_id(unsigned char id[128]) {
   API_BEGIN
   nccl_unique_id(id);
@@ -264,6 +293,7 @@ int lbcu_ctx_create(lbcu_world w, int rank, int device, const int global[4], con
   LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
   LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_comm, cudaEventDisableTiming));
   for (auto& e : ctx->ev) LBCU_CUDA(cudaEventCreate(&e));
+  w->t->attach(rank, device);
   ctx->max_partials = static_cast<int>(2 * ((g.vh + 31) / 32) + 4096);  // hop blocks >= 32 threads
   LBCU_CUDA(cudaMalloc(&ctx->partials, sizeof(double) * 2 * ctx->max_partials));
   LBCU_CUDA(cudaMalloc(&ctx->ticket, sizeof(unsigned) * 4));

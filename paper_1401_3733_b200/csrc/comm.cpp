@@ -12,8 +12,26 @@
 //             halos, ncclAllReduce(double, sum) for CG scalars, all on the
 //             context stream (NVLink 5 / NVSwitch). libnccl is dlopen()ed on
 //             first use so single-GPU users never load it.
+//   ipc     : one process per GPU on one node, direct halos: every rank maps
+//             the peers' receive arenas (cudaIpcOpenMemHandle) and the halo
+//             pack kernel stores its records straight into them over NVLink;
+//             completion travels as an interprocess CUDA event per exchange,
+//             recorded after the pack and waited on (stream-ordered) before
+//             the boundary kernel. A host barrier in a POSIX shared-memory
+//             segment separates the record and the wait of each exchange, so
+//             no kernel ever spins on another rank. The thread world has the
+//             same direct mode (one process, plain pointers) for testing.
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <map>
+#include <thread>
 
 #include <condition_variable>
 #include <cstring>
@@ -37,9 +55,44 @@ struct SingleTransport final : Transport {
 };
 
 struct ThreadTransport final : Transport {
-  explicit ThreadTransport(int n) : n_(n), contrib_(n), posted_(n) {}
+  ThreadTransport(int n, bool direct) : n_(n), direct_(direct), contrib_(n), posted_(n), events_(n) {}
+  ~ThreadTransport() override {
+    for (auto& ev : events_)
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+  }
   int nranks() const override { return n_; }
   bool capturable() const override { return false; }
+
+  // ---- direct mode (peer arenas are plain device pointers in one process)
+  bool direct() const override { return direct_; }
+  void set_direct(bool on) override { direct_ = on; }
+  void attach(int rank, int) override {
+    if (!direct_) return;
+    for (auto& e : events_[rank])
+      if (!e) LBCU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  void map_arena(int rank, int key, void* local, size_t) override {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      auto& v = arenas_[key];
+      if (v.empty()) v.assign(n_, nullptr);
+      v[rank] = local;
+    }
+    sync();
+  }
+  void* peer_arena(int, int key, int peer) const override {
+    std::lock_guard<std::mutex> lk(m_);
+    auto it = arenas_.find(key);
+    return it == arenas_.end() ? nullptr : it->second[peer];
+  }
+  void post(int rank, long long epoch, cudaStream_t s) override {
+    LBCU_CUDA(cudaEventRecord(events_[rank][epoch & 1], s));
+  }
+  void await(int, long long epoch, const std::vector<int>& peers, cudaStream_t s) override {
+    sync();  // every rank has recorded this epoch's event
+    for (int q : peers) LBCU_CUDA(cudaStreamWaitEvent(s, events_[q][epoch & 1], 0));
+  }
 
   // generation barrier (transport.cpp:28-55, without op tagging)
   void sync() {
@@ -100,12 +153,15 @@ struct ThreadTransport final : Transport {
     return tree(k, lo, mid) + tree(k, mid, hi);
   }
   int n_;
-  std::mutex m_;
+  bool direct_;
+  mutable std::mutex m_;
   std::condition_variable cv_;
   int arrived_ = 0;
   uint64_t phase_ = 0;
   std::vector<std::vector<double>> contrib_;
   std::vector<std::vector<Msg>> posted_;
+  std::vector<std::array<cudaEvent_t, 2>> events_;
+  std::map<int, std::vector<void*>> arenas_;
 };
 
 // ---- NCCL through dlopen ----------------------------------------------------
@@ -206,12 +262,195 @@ struct NcclTransport final : Transport {
   double* scratch_ = nullptr;
 };
 
+// ---- one process per GPU, peer-memory halos through CUDA IPC ---------------
+constexpr int kIpcMaxRanks = 8;  // one node
+constexpr int kIpcMaxKeys = 16;  // arenas (one per representation dimension)
+constexpr int kIpcMaxSum = 8;    // doubles per host-path allreduce
+constexpr uint64_t kIpcMagic = 0x6c6263752d697063ULL;
+
+struct IpcShared {
+  std::atomic<uint64_t> magic;
+  std::atomic<uint32_t> arrive;
+  std::atomic<uint32_t> gen;
+  std::atomic<uint32_t> attached;
+  cudaIpcEventHandle_t ev[kIpcMaxRanks][2];
+  cudaIpcMemHandle_t mem[kIpcMaxKeys][kIpcMaxRanks];
+  double sum[kIpcMaxRanks][kIpcMaxSum];
+};
+
+struct IpcTransport final : Transport {
+  IpcTransport(int n, int rank, const char* name, const unsigned char* nccl_id) : n_(n), rank_(rank), name_(name) {
+    if (n < 1 || n > kIpcMaxRanks) throw Error(LBCU_CONFIG_ERROR, "ipc world: 1..8 ranks on one node");
+    if (rank < 0 || rank >= n) throw Error(LBCU_CONTRACT_VIOLATION, "ipc world: rank out of range");
+    if (!name || name[0] != '/') throw Error(LBCU_CONFIG_ERROR, "ipc world: segment name must start with '/'");
+    if (nccl_id) inner_ = make_nccl_transport(n, rank, nccl_id);
+    const size_t bytes = sizeof(IpcShared);
+    int fd = -1;
+    if (rank == 0) {
+      shm_unlink(name);  // a stale segment of an earlier run
+      fd = shm_open(name, O_CREAT | O_EXCL | O_RDWR, 0600);
+      if (fd < 0 || ftruncate(fd, bytes) != 0) throw Error(LBCU_TRANSPORT_ERROR, "ipc world: shm_open/ftruncate failed");
+    } else {
+      const auto t0 = std::chrono::steady_clock::now();
+      while ((fd = shm_open(name, O_RDWR, 0600)) < 0) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+          throw Error(LBCU_TRANSPORT_ERROR, "ipc world: rank 0 never created the segment");
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+      }
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw Error(LBCU_TRANSPORT_ERROR, "ipc world: mmap failed");
+    sh_ = static_cast<IpcShared*>(p);
+    if (rank == 0) {
+      sh_->arrive.store(0);
+      sh_->gen.store(0);
+      sh_->attached.store(0);
+      sh_->magic.store(kIpcMagic, std::memory_order_release);
+    } else {
+      wait_until([&] { return sh_->magic.load(std::memory_order_acquire) == kIpcMagic; });
+    }
+    sh_->attached.fetch_add(1);
+    wait_until([&] { return sh_->attached.load() == static_cast<uint32_t>(n_); });
+    host_barrier();
+    if (rank == 0) shm_unlink(name);  // every rank holds the mapping now
+  }
+  ~IpcTransport() override {
+    // collective teardown: nobody closes its mappings while a peer may still
+    // be inside a collective call (bounded wait, never throws)
+    if (sh_) {
+      const uint32_t g = sh_->gen.load(std::memory_order_acquire);
+      if (sh_->arrive.fetch_add(1, std::memory_order_acq_rel) + 1 == static_cast<uint32_t>(n_)) {
+        sh_->arrive.store(0, std::memory_order_relaxed);
+        sh_->gen.fetch_add(1, std::memory_order_release);
+      } else {
+        const auto t0 = std::chrono::steady_clock::now();
+        while (sh_->gen.load(std::memory_order_acquire) == g &&
+               std::chrono::steady_clock::now() - t0 < std::chrono::seconds(30))
+          sched_yield();
+      }
+    }
+    for (auto& kv : peer_mem_)
+      for (void* q : kv.second)
+        if (q) cudaIpcCloseMemHandle(q);
+    for (int q = 0; q < n_; ++q)
+      for (int e = 0; e < 2; ++e)
+        if (ev_[q][e]) cudaEventDestroy(ev_[q][e]);
+    if (sh_) munmap(sh_, sizeof(IpcShared));
+  }
+  int nranks() const override { return n_; }
+  bool capturable() const override { return false; }
+  bool direct() const override { return direct_; }
+  void set_direct(bool on) override {
+    if (!on && !inner_) throw Error(LBCU_TRANSPORT_ERROR, "ipc world without NCCL: halos must be direct");
+    direct_ = on;
+  }
+  void bind_device(int device) override {
+    if (inner_) inner_->bind_device(device);
+  }
+  void attach(int rank, int) override {
+    if (attached_) return;
+    for (int e = 0; e < 2; ++e) {
+      LBCU_CUDA(cudaEventCreateWithFlags(&ev_[rank][e], cudaEventDisableTiming | cudaEventInterprocess));
+      LBCU_CUDA(cudaIpcGetEventHandle(&sh_->ev[rank][e], ev_[rank][e]));
+    }
+    host_barrier();
+    for (int q = 0; q < n_; ++q)
+      if (q != rank)
+        for (int e = 0; e < 2; ++e) LBCU_CUDA(cudaIpcOpenEventHandle(&ev_[q][e], sh_->ev[q][e]));
+    host_barrier();
+    attached_ = true;
+  }
+  void map_arena(int rank, int key, void* local, size_t) override {
+    if (key < 0 || key >= kIpcMaxKeys) throw Error(LBCU_TRANSPORT_ERROR, "ipc world: arena key out of range");
+    LBCU_CUDA(cudaIpcGetMemHandle(&sh_->mem[key][rank], local));
+    host_barrier();
+    auto& v = peer_mem_[key];
+    v.assign(n_, nullptr);
+    for (int q = 0; q < n_; ++q)
+      if (q != rank)
+        LBCU_CUDA(cudaIpcOpenMemHandle(&v[q], sh_->mem[key][q], cudaIpcMemLazyEnablePeerAccess));
+    v[rank] = local;
+    host_barrier();
+  }
+  void* peer_arena(int, int key, int peer) const override {
+    auto it = peer_mem_.find(key);
+    return it == peer_mem_.end() ? nullptr : it->second[peer];
+  }
+  void post(int rank, long long epoch, cudaStream_t s) override {
+    LBCU_CUDA(cudaEventRecord(ev_[rank][epoch & 1], s));
+  }
+  void await(int, long long epoch, const std::vector<int>& peers, cudaStream_t s) override {
+    host_barrier();  // every rank has recorded this epoch's event
+    for (int q : peers) LBCU_CUDA(cudaStreamWaitEvent(s, ev_[q][epoch & 1], 0));
+  }
+  void allreduce(int rank, double* dev, int n, cudaStream_t s) override {
+    if (n_ == 1) return;
+    if (inner_) return inner_->allreduce(rank, dev, n, s);
+    if (n > kIpcMaxSum) throw Error(LBCU_TRANSPORT_ERROR, "ipc world: host sum of more than 8 values");
+    double loc[kIpcMaxSum];
+    LBCU_CUDA(cudaMemcpyAsync(loc, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    LBCU_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k < n; ++k) sh_->sum[rank][k] = loc[k];
+    host_barrier();
+    for (int k = 0; k < n; ++k) loc[k] = tree(k, 0, n_);  // fixed order on every rank
+    host_barrier();
+    LBCU_CUDA(cudaMemcpyAsync(dev, loc, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    LBCU_CUDA(cudaStreamSynchronize(s));
+  }
+  void exchange(int rank, const std::vector<Msg>& msgs, cudaStream_t s) override {
+    if (!inner_) throw Error(LBCU_TRANSPORT_ERROR, "ipc world: message exchange needs NCCL");
+    inner_->exchange(rank, msgs, s);
+  }
+  void barrier(int) override { host_barrier(); }
+
+ private:
+  template <class F>
+  void wait_until(F&& ready) {
+    const auto t0 = std::chrono::steady_clock::now();
+    unsigned spins = 0;
+    while (!ready()) {
+      if (++spins > 4096) {
+        sched_yield();
+        if ((spins & 0xffff) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(600))
+          throw Error(LBCU_TRANSPORT_ERROR, "ipc world: host barrier timed out");
+      }
+    }
+  }
+  // generation barrier over the shared segment
+  void host_barrier() {
+    const uint32_t g = sh_->gen.load(std::memory_order_acquire);
+    if (sh_->arrive.fetch_add(1, std::memory_order_acq_rel) + 1 == static_cast<uint32_t>(n_)) {
+      sh_->arrive.store(0, std::memory_order_relaxed);
+      sh_->gen.fetch_add(1, std::memory_order_release);
+      return;
+    }
+    wait_until([&] { return sh_->gen.load(std::memory_order_acquire) != g; });
+  }
+  double tree(int k, int lo, int hi) const {
+    if (hi - lo == 1) return sh_->sum[lo][k];
+    const int mid = lo + (hi - lo) / 2;
+    return tree(k, lo, mid) + tree(k, mid, hi);
+  }
+  int n_, rank_;
+  std::string name_;
+  IpcShared* sh_ = nullptr;
+  std::unique_ptr<Transport> inner_;
+  cudaEvent_t ev_[kIpcMaxRanks][2] = {};
+  bool attached_ = false;
+  bool direct_ = true;
+  std::map<int, std::vector<void*>> peer_mem_;
+};
+
 }  // namespace
 
 std::unique_ptr<Transport> make_single_transport() { return std::make_unique<SingleTransport>(); }
-std::unique_ptr<Transport> make_thread_transport(int n) {
+std::unique_ptr<Transport> make_thread_transport(int n, bool direct) {
   if (n < 1) throw Error(LBCU_CONFIG_ERROR, "thread world needs >= 1 rank");
-  return std::make_unique<ThreadTransport>(n);
+  return std::make_unique<ThreadTransport>(n, direct);
+}
+std::unique_ptr<Transport> make_ipc_transport(int n, int rank, const char* name, const unsigned char* nccl_id) {
+  return std::make_unique<IpcTransport>(n, rank, name, nccl_id);
 }
 std::unique_ptr<Transport> make_nccl_transport(int n, int rank, const unsigned char id[128]) {
   return std::make_unique<NcclTransport>(n, rank, id);

@@ -24,6 +24,7 @@
 //   face dir 0 (to -mu partner): h = (1 - g_mu) projection of in at x_mu = 0
 //   face dir 1 (to +mu partner): g = U_mu(y)^dag (1 + g_mu) projection at
 //                                x_mu = L_mu - 1 (no gauge halo needed).
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -655,6 +656,16 @@ HaloBufs& halo_bufs(lbcu_ctx_s* ctx, int dr) {
   HaloBufs& hb = ctx->halo[dr];
   size_t need = 0;
   for (int f = 0; f < 8; ++f) need = std::max<size_t>(need, 2 * dr * ctx->plan.count[f]);
+  Transport* T = ctx->world->t.get();
+  if (T->direct()) {  // collective on first use per dr: every rank maps every arena
+    if (!hb.arena) {
+      hb.slot = (need + 31) / 32 * 32;
+      const size_t bytes = 2 * 8 * 2 * hb.slot * sizeof(double2);
+      LBCU_CUDA(cudaMalloc(&hb.arena, bytes));
+      T->map_arena(ctx->rank, dr, hb.arena, bytes);
+    }
+    return hb;
+  }
   if (hb.cap < need) {
     for (int p = 0; p < 2; ++p)
       for (int f = 0; f < 8; ++f) {
@@ -752,6 +763,10 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   HaloBufs& hb = halo_bufs(ctx, dr);
   if (c.post != POST_NONE)
     throw Error(LBCU_CONTRACT_VIOLATION, "fused CG scalar steps need a single rank");
+  Transport* T = ctx->world->t.get();
+  const bool direct = T->direct();
+  const long long epoch = ctx->xepoch++;
+  auto arena_off = [&](int p, int f) { return ((p * 8 + f) * 2 + (epoch & 1)) * hb.slot; };
   PackAll PA{};
   std::vector<Transport::Msg> msgs;
   int pack_blocks = 0;
@@ -772,7 +787,13 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       P.bc_kernel = A.bc_kernel;
       P.t_off = A.t_off;
       P.bc_tlast = A.bc_tlast;
-      P.outbuf = hb.send[p][f];
+      if (direct) {  // straight into the receiving rank's arena slot [p][f ^ 1][epoch]
+        auto* peer = static_cast<double2*>(T->peer_arena(ctx->rank, dr, ctx->plan.partner[f]));
+        if (!peer) throw Error(LBCU_TRANSPORT_ERROR, "direct halo: peer arena not mapped");
+        P.outbuf = peer + arena_off(p, f ^ 1);
+      } else {
+        P.outbuf = hb.send[p][f];
+      }
       PA.first[PA.njobs] = pack_blocks;
       pack_blocks += (P.count + kBlock - 1) / kBlock;
       PA.njobs++;
@@ -820,8 +841,11 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     return G;
   };
   // interior sites (no halo dependency) run on the compute stream while the
-  // halos travel on the comm stream; boundary sites wait for both.
-  LBCU_CUDA(cudaEventRecord(ctx->ev_pack, s));
+  // halos travel; boundary sites wait for them. Direct transports: the pack
+  // kernel already stored into the peers, its completion is posted as an
+  // event that the peers' streams wait on before their boundary launch.
+  if (direct) T->post(ctx->rank, epoch, s);
+  else LBCU_CUDA(cudaEventRecord(ctx->ev_pack, s));
   for (int gi = 0; gi < ngroups; ++gi) {
     HopArgs Ai = group_args(gi, false);
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
@@ -829,18 +853,26 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     });
     ctx->launches += 1;
   }
-  LBCU_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_pack, 0));
-  ctx->world->t->exchange(ctx->rank, msgs, ctx->comm_stream);
-  LBCU_CUDA(cudaEventRecord(ctx->ev_comm, ctx->comm_stream));
-  LBCU_CUDA(cudaStreamWaitEvent(s, ctx->ev_comm, 0));
+  if (direct) {
+    std::vector<int> peers;
+    for (int f = 0; f < 8; ++f)
+      if (ctx->plan.count[f] && std::find(peers.begin(), peers.end(), ctx->plan.partner[f]) == peers.end())
+        peers.push_back(ctx->plan.partner[f]);
+    T->await(ctx->rank, epoch, peers, s);
+  } else {
+    LBCU_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_pack, 0));
+    T->exchange(ctx->rank, msgs, ctx->comm_stream);
+    LBCU_CUDA(cudaEventRecord(ctx->ev_comm, ctx->comm_stream));
+    LBCU_CUDA(cudaStreamWaitEvent(s, ctx->ev_comm, 0));
+  }
   for (int gi = 0; gi < ngroups; ++gi) {
     HopArgs Ab = group_args(gi, true);
     for (int pp = 0; pp < 2; ++pp)
       for (int mu = 0; mu < 4; ++mu) {
         // recv[2 mu + 1] holds the +mu partner's dir-0 face (forward halo),
         // recv[2 mu] the -mu partner's dir-1 face (backward halo)
-        Ab.hfwd[pp][mu] = hb.recv[pp][2 * mu + 1];
-        Ab.hbwd[pp][mu] = hb.recv[pp][2 * mu + 0];
+        Ab.hfwd[pp][mu] = direct ? hb.arena + arena_off(pp, 2 * mu + 1) : hb.recv[pp][2 * mu + 1];
+        Ab.hbwd[pp][mu] = direct ? hb.arena + arena_off(pp, 2 * mu + 0) : hb.recv[pp][2 * mu + 0];
         Ab.hcount[mu] = static_cast<int>(ctx->plan.count[2 * mu]);
       }
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {

@@ -86,10 +86,38 @@ struct Transport {
   virtual void barrier(int rank) = 0;
   // called by each context after it selected its device
   virtual void bind_device(int /*device*/) {}
+  // called by each context once its stream exists (rank known)
+  virtual void attach(int /*rank*/, int /*device*/) {}
+
+  // ---- direct halo exchange over peer memory -----------------------------
+  // With a direct transport the halo pack kernel stores its records straight
+  // into the receiving rank's arena (P2P stores over NVLink for the IPC
+  // world), so pack and transfer are one kernel; no send buffers, no copies.
+  virtual bool direct() const { return false; }
+  // switch a direct transport to message exchange and back (collective;
+  // the IPC world then uses its NCCL communicator for the halos)
+  virtual void set_direct(bool on) {
+    if (on) throw Error(LBCU_TRANSPORT_ERROR, "transport has no direct halo mode");
+  }
+  // collective, once per key: register this rank's receive arena and map
+  // every peer's (same size and layout on every rank)
+  virtual void map_arena(int /*rank*/, int /*key*/, void* /*local*/, size_t /*bytes*/) {
+    throw Error(LBCU_TRANSPORT_ERROR, "transport has no peer-memory arenas");
+  }
+  virtual void* peer_arena(int /*rank*/, int /*key*/, int /*peer*/) const { return nullptr; }
+  // after the pack kernel of exchange `epoch`: publish its completion
+  virtual void post(int /*rank*/, long long /*epoch*/, cudaStream_t /*s*/) {}
+  // order stream s after every listed peer's post of exchange `epoch`
+  virtual void await(int /*rank*/, long long /*epoch*/, const std::vector<int>& /*peers*/, cudaStream_t /*s*/) {}
 };
 
 std::unique_ptr<Transport> make_single_transport();
-std::unique_ptr<Transport> make_thread_transport(int nranks);
+std::unique_ptr<Transport> make_thread_transport(int nranks, bool direct = false);
+// one process per rank on one node: peer-memory halos through CUDA IPC, a
+// POSIX shared-memory segment `name` for the bootstrap and the host barrier;
+// CG sums through NCCL when `nccl_id` is given, else through the segment
+std::unique_ptr<Transport> make_ipc_transport(int nranks, int rank, const char* name,
+                                              const unsigned char* nccl_id);
 std::unique_ptr<Transport> make_nccl_transport(int nranks, int rank, const unsigned char id[128]);
 void nccl_unique_id(unsigned char id[128]);
 

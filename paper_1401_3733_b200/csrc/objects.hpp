@@ -41,6 +41,10 @@ enum Epi { EPI_STORE = 0, EPI_STORE_NORM = 1, EPI_CG = 2 };
 struct HaloBufs {
   double2* send[2][8] = {};  // by output parity, face
   double2* recv[2][8] = {};
+  // direct transports: one receive arena [parity][face][epoch & 1] of `slot`
+  // double2 each, mapped by every peer (Transport::map_arena)
+  double2* arena = nullptr;
+  size_t slot = 0;
   size_t cap = 0;  // double2 per buffer
 };
 
@@ -76,6 +80,7 @@ struct lbcu_ctx_s {
   void* staging = nullptr;  // device staging buffer for host<->device layout transposes
   size_t staging_bytes = 0;
   long long launches = 0;
+  long long xepoch = 0;  // halo exchanges so far (direct transports: arena / event slot)
   cudaEvent_t ev_cg[2] = {nullptr, nullptr};  // per-iteration CG state copies (host loop)
   // host-field pipeline (lbcu_dphi_host): 2 slots, copy-in / copy-out streams
   struct HostPipe {

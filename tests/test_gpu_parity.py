@@ -212,16 +212,19 @@ def test_tampered_operator_fails_consistency():
         pass
 
 
+@pytest.mark.parametrize("direct", [False, True], ids=["copy", "direct"])
 @pytest.mark.parametrize("grid", [(2, 1, 1, 1), (2, 1, 1, 2), (1, 2, 2, 1)], ids=["t2", "t2z2", "x2y2"])
 @pytest.mark.parametrize("n,rep", [REPS[0], REPS[3]], ids=[REP_IDS[0], REP_IDS[3]])
-def test_decomposed_dphi_matches_single(grid, n, rep):
+def test_decomposed_dphi_matches_single(grid, n, rep, direct):
     """Serial oracle vs decomposition: ranks as host threads on one GPU,
-    half-spinor halos packed by kernels and exchanged by the thread transport."""
+    half-spinor halos packed by kernels and exchanged by the thread transport
+    (copy: buffers copied between barriers; direct: the pack kernel stores
+    into the receiving rank's arena, event + host barrier per exchange)."""
     L = [8, 4, 4, 8]
     dr, g, s = fields(L, n, rep)
     want = O.port_dirac(L, 1, 0.1, g, s)
     nranks = int(np.prod(grid))
-    world = lb.World.threads(nranks)
+    world = lb.World.threads(nranks, direct=direct)
 
     def body(r):
         ctx = lb.Context(L, grid, r, 0, world)
@@ -238,13 +241,14 @@ def test_decomposed_dphi_matches_single(grid, n, rep):
     assert rel_l2(got, want) < 1e-14
 
 
-def test_decomposed_cg_eo_matches_single():
+@pytest.mark.parametrize("direct", [False, True], ids=["copy", "direct"])
+def test_decomposed_cg_eo_matches_single(direct):
     L = [8, 4, 4, 8]
     n, rep = 3, lb.FUNDAMENTAL
     dr, g, s = fields(L, n, rep)
     ref = O.ref_cg_eo(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s, 1e-10)
     grid = (2, 1, 1, 2)
-    world = lb.World.threads(4)
+    world = lb.World.threads(4, direct=direct)
 
     def body(r):
         ctx = lb.Context(L, grid, r, 0, world)
@@ -342,3 +346,32 @@ def test_cg_host_loop_matches_graph(solver, monkeypatch):
     # a tolerance reached at the iteration cap: the loop stops at max_iterations
     with pytest.raises(lb.NonConvergence):
         run(gauge, 0.1, rhs, lb.CgSettings(1e-10, a.iterations - 2))
+
+
+def test_direct_halo_toggle_matches():
+    """A direct thread world switched to message exchange and back
+    (lbcu_world_set_direct, as bench.py's IPC/NCCL cross-check does) gives
+    the same decomposed Dphi bit for bit in every mode."""
+    L, grid = [8, 4, 4, 8], (2, 1, 1, 2)
+    n, rep = 2, lb.FUNDAMENTAL
+    dr, g, s = fields(L, n, rep)
+    world = lb.World.threads(4, direct=True)
+
+    def body(r):
+        ctx = lb.Context(L, grid, r, 0, world)
+        idx = global_index(L, grid, r)
+        gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g[idx])
+        inp = lb.SpinorField(ctx, dr).upload(s[idx])
+        out = lb.SpinorField(ctx, dr)
+        res = []
+        for mode in (True, False, True):
+            ctx.barrier()
+            if r == 0:
+                world.set_direct(mode)
+            ctx.barrier()
+            lb.apply_dirac(out, gauge, inp, 0.1)
+            res.append(out.download())
+        return res
+
+    for res in run_ranks(4, body):
+        assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
