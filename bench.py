@@ -250,10 +250,16 @@ def run_gpu(args, cfg):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         import uuid
-        obj = [(lb.World.nccl_unique_id(), f"/lbcu_{uuid.uuid4().hex[:16]}") if rank == 0 else None]
+        if args.emulate:  # test mode: every rank on GPU 0, gloo, no NCCL at all
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [(None if args.emulate else lb.World.nccl_unique_id(), f"/lbcu_{uuid.uuid4().hex[:16]}")
+               if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid, shm_name = obj[0]
         # halos: direct peer-memory stores by the pack kernel (IPC world; NCCL
@@ -267,6 +273,8 @@ def run_gpu(args, cfg):
             except Exception as e:  # noqa: BLE001
                 transport = f"nccl (ipc world unavailable: {e})"
         if world is None:
+            if args.emulate:
+                raise SystemExit(f"--emulate needs the IPC world: {transport}")
             world = lb.World.nccl(ws, rank, uid)
     dr = lb.rep_dim(rep, n)
     real = lb.rep_is_real(rep)
@@ -286,7 +294,9 @@ def run_gpu(args, cfg):
     fmt, fmt_err = gauge.storage()
     a = lb.SpinorField(ctx, dr).upload(s)
     b = lb.SpinorField(ctx, dr)
-    if ws > 1 and transport == "ipc":
+    if ws > 1 and transport == "ipc" and args.emulate:
+        transport = "ipc (emulated ranks sharing GPU 0, host CG sums; timings meaningless)"
+    elif ws > 1 and transport == "ipc":
         # the direct halos must reproduce the NCCL send/recv halos bit for bit
         lb.apply_dirac(b, gauge, a, mass)
         world.set_direct(False)
@@ -312,7 +322,7 @@ def run_gpu(args, cfg):
         if dist is None:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if args.emulate else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -469,6 +479,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dense-links", action="store_true", help="store links as dense matrices")
     ap.add_argument("--host-links", action="store_true", help="generate links on the host and upload")
+    ap.add_argument("--emulate", action="store_true",
+                    help="test the N > 1 flow with every rank on GPU 0 (gloo, IPC world, no NCCL); "
+                         "correctness only, the timings are meaningless")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
