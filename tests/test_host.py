@@ -253,3 +253,38 @@ def test_two_rank_gloo_halo_exchange():
             p.join(120)
             assert p.exitcode == 0
         assert result[0] and result[1]
+
+
+def _ipc_bootstrap(rank, nranks, name, q):
+    import paper_1401_3733_b200 as lbm
+    try:
+        w = lbm.World.ipc(nranks, rank, name)  # shared-memory bootstrap + barrier, no CUDA call
+        w.close()                              # collective teardown barrier
+        q.put((rank, "ok"))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+
+
+def test_ipc_world_bootstrap_on_host():
+    """lbcu_world_ipc's POSIX shared-memory bootstrap (rank 0 creates the
+    segment, the others attach), its generation barrier and its collective
+    teardown, across three processes; the segment name is unlinked once every
+    rank holds the mapping. Bad arguments fail with a config error."""
+    import multiprocessing as mp
+    import uuid
+
+    name = f"/lbcu_host_{uuid.uuid4().hex[:12]}"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ipc_bootstrap, args=(r, 3, name, q)) for r in range(3)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok", 2: "ok"}
+    assert not os.path.exists("/dev/shm" + name)
+    with pytest.raises(lb.ConfigError):
+        lb.World.ipc(2, 0, "no-leading-slash")
+    with pytest.raises(lb.ConfigError):
+        lb.World.ipc(9, 0, "/lbcu_too_many")
