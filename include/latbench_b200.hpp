@@ -108,6 +108,22 @@ class WorkerGroup {
     check(lbcu_world_nccl(nranks, rank, id, &w));
     return std::shared_ptr<WorkerGroup>(new WorkerGroup(w));
   }
+  // one process per GPU on one node; halos stored by the pack kernel into the
+  // neighbour's arena over NVLink (CUDA IPC). shm_name: "/..." unique per job;
+  // nccl_id (nullable): NCCL for the CG sums.
+  static std::shared_ptr<WorkerGroup> ipc(int nranks, int rank, const std::string& shm_name,
+                                          const unsigned char* nccl_id = nullptr) {
+    lbcu_world w = nullptr;
+    check(lbcu_world_ipc(nranks, rank, shm_name.c_str(), nccl_id, &w));
+    return std::shared_ptr<WorkerGroup>(new WorkerGroup(w));
+  }
+  // in-process ranks with the same direct halo protocol
+  static std::shared_ptr<WorkerGroup> threads_direct(int nranks) {
+    lbcu_world w = nullptr;
+    check(lbcu_world_threads_direct(nranks, &w));
+    return std::shared_ptr<WorkerGroup>(new WorkerGroup(w));
+  }
+  void set_direct(bool on) { check(lbcu_world_set_direct(w_, on ? 1 : 0)); }
   ~WorkerGroup() { lbcu_world_destroy(w_); }
   lbcu_world handle() const { return w_; }
 
