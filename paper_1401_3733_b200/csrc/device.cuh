@@ -184,6 +184,77 @@ struct Reduce {
   int use_graph;
 };
 
+// Split form for the hop kernels (measured: profiles/r03_cgvar*): each block
+// only writes its partial (no fence, no ticket, so it retires as soon as its
+// warps are done), and k_reduce_finish, launched after the last contributing
+// launch, sums the partials in a fixed order and runs the CG step. The
+// fence + atomic + second barrier of the last-block form kept every block's
+// registers idle for ~2 us and cost 20-29 us per 0.5 M-site eo hop.
+template <int NR>
+__device__ __forceinline__ void block_reduce_partial(const Reduce& R, double (&v)[NR]) {
+  __shared__ double sh[32][NR];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < NR; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) sh[warp][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < nwarps; ++w) s += sh[w][k];
+      R.part[(size_t)(R.offset + blockIdx.x) * NR + k] = s;
+    }
+  }
+}
+
+constexpr int kFinishThreads = 1024;
+
+template <int NR>
+__global__ void __launch_bounds__(kFinishThreads) k_reduce_finish(const Reduce R) {
+  __shared__ double sh[kFinishThreads / 32][NR];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) acc[k] = 0.0;
+  // 8 independent loads in flight per thread, then a fixed-order sum
+  constexpr int U = 8;
+  for (int base = 0; base < R.total_blocks; base += U * kFinishThreads) {
+    double v[U][NR];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int b = base + j * kFinishThreads + threadIdx.x;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) v[j][k] = b < R.total_blocks ? R.part[(size_t)b * NR + k] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+#pragma unroll
+      for (int k = 0; k < NR; ++k) acc[k] += v[j][k];
+  }
+#pragma unroll
+  for (int k = 0; k < NR; ++k)
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) sh[warp][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < kFinishThreads / 32; ++w) s += sh[w][k];
+      R.result[k] = s;
+    }
+    if (R.post == POST_ALPHA) cg_post_alpha(R.cg, R.result[0]);
+    else if (R.post == POST_END) cg_post_end(R.cg, R.result[0], R.hist, R.handle, R.use_graph);
+  }
+}
+
 template <int NR>
 __device__ __forceinline__ void block_reduce_finalize(const Reduce& R, double (&v)[NR]) {
   __shared__ double sh[32][NR];

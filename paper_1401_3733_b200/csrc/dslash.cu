@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ 
   } else {
     if (ok) site_body<D, REAL, FMT, BND, EPI, ZS>(A, par, idx, nrm, 0u);
   }
-  if constexpr (EPI != EPI_STORE) block_reduce_finalize<1>(A.red, nrm);
+  if constexpr (EPI != EPI_STORE) block_reduce_partial<1>(A.red, nrm);
 }
 
 template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS>
@@ -752,6 +752,10 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s, blocks, zs);
     });
     ctx->launches += 1;
+    if (reduce) {
+      k_reduce_finish<1><<<1, kFinishThreads, 0, s>>>(A.red);
+      ctx->launches += 1;
+    }
     LBCU_CUDA(cudaGetLastError());
     return;
   }
@@ -878,6 +882,11 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
       launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ab, true, c.epi, Ab.nsites, joint ? 2 : 1, s);
     });
+    ctx->launches += 1;
+  }
+  if (reduce) {  // all interior and boundary partials are in place
+    Reduce R{ctx->partials, ctx->ticket, c.result, 0, total_blocks};
+    k_reduce_finish<1><<<1, kFinishThreads, 0, s>>>(R);
     ctx->launches += 1;
   }
   LBCU_CUDA(cudaGetLastError());
