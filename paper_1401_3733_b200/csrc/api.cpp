@@ -296,8 +296,6 @@ int lbcu_ctx_create(lbcu_world w, int rank, int device, const int global[4], con
   w->t->attach(rank, device);
   ctx->max_partials = static_cast<int>(2 * ((g.vh + 31) / 32) + 4096);  // hop blocks >= 32 threads
   LBCU_CUDA(cudaMalloc(&ctx->partials, sizeof(double) * 2 * ctx->max_partials));
-  LBCU_CUDA(cudaMalloc(&ctx->ticket, sizeof(unsigned) * 4));
-  LBCU_CUDA(cudaMemset(ctx->ticket, 0, sizeof(unsigned) * 4));
   LBCU_CUDA(cudaMalloc(&ctx->dscal, sizeof(double) * 64));
   LBCU_CUDA(cudaMemset(ctx->dscal, 0, sizeof(double) * 64));
   LBCU_CUDA(cudaMallocHost(&ctx->hscal, sizeof(double) * 64));
@@ -352,7 +350,6 @@ int lbcu_ctx_destroy(lbcu_ctx c) {
     if (c->blist[p]) cudaFree(c->blist[p]);
   }
   cudaFree(c->partials);
-  cudaFree(c->ticket);
   cudaFree(c->dscal);
   cudaFreeHost(c->hscal);
   cudaFree(c->dcg);

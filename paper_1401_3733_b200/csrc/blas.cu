@@ -30,7 +30,7 @@ __global__ void k_sqnorm(const double2* __restrict__ a, size_t n, Reduce R) {
     const double2 z = __ldg(a + i);
     v[0] = fma(z.x, z.x, fma(z.y, z.y, v[0]));
   }
-  block_reduce_finalize<1>(R, v);
+  block_reduce_partial<1>(R, v);
 }
 
 // sum conj(a) b
@@ -41,7 +41,7 @@ __global__ void k_dot(const double2* __restrict__ a, const double2* __restrict__
     v[0] = fma(x.x, y.x, fma(x.y, y.y, v[0]));
     v[1] = fma(x.x, y.y, fma(-x.y, y.x, v[1]));
   }
-  block_reduce_finalize<2>(R, v);
+  block_reduce_partial<2>(R, v);
 }
 
 // y += a x
@@ -104,7 +104,7 @@ __global__ void k_cg_r(double2* __restrict__ r, const double2* __restrict__ ap, 
     r[i] = rv;
     v[0] = fma(rv.x, rv.x, fma(rv.y, rv.y, v[0]));
   }
-  block_reduce_finalize<1>(R, v);
+  block_reduce_partial<1>(R, v);
 }
 
 __global__ void k_cg_xfinal(double2* __restrict__ x, const double2* __restrict__ p, size_t n,
@@ -220,20 +220,22 @@ void ensure_staging(lbcu_ctx_s* ctx, size_t bytes) {
 }  // namespace
 
 static Reduce make_reduce(lbcu_ctx_s* ctx, double* res, int blocks) {
-  return Reduce{ctx->partials, ctx->ticket, res, 0, blocks};
+  return Reduce{ctx->partials, res, 0, blocks};
 }
 
 void blas_sqnorm(lbcu_ctx_s* ctx, const lbcu_spinor_s* f, double* dres) {
   const int nb = flat_blocks(ctx, f->elems);
   k_sqnorm<<<nb, kThreads, 0, ctx->stream>>>(f->base, f->elems, make_reduce(ctx, dres, nb));
-  ctx->launches++;
+  k_reduce_finish<1><<<1, kFinishThreads, 0, ctx->stream>>>(make_reduce(ctx, dres, nb));
+  ctx->launches += 2;
   LBCU_CUDA(cudaGetLastError());
 }
 
 void blas_dot(lbcu_ctx_s* ctx, const lbcu_spinor_s* a, const lbcu_spinor_s* b, double* dres2) {
   const int nb = flat_blocks(ctx, a->elems);
   k_dot<<<nb, kThreads, 0, ctx->stream>>>(a->base, b->base, a->elems, make_reduce(ctx, dres2, nb));
-  ctx->launches++;
+  k_reduce_finish<2><<<1, kFinishThreads, 0, ctx->stream>>>(make_reduce(ctx, dres2, nb));
+  ctx->launches += 2;
   LBCU_CUDA(cudaGetLastError());
 }
 
@@ -276,7 +278,8 @@ void cg_p_update(lbcu_ctx_s* ctx, lbcu_spinor_s* p, const lbcu_spinor_s* r, lbcu
 void cg_r_update(lbcu_ctx_s* ctx, lbcu_spinor_s* r, const lbcu_spinor_s* ap, double* dres) {
   const int nb = flat_blocks(ctx, r->elems);
   k_cg_r<<<nb, kThreads, 0, ctx->stream>>>(r->base, ap->base, r->elems, ctx->dcg, make_reduce(ctx, dres, nb));
-  ctx->launches++;
+  k_reduce_finish<1><<<1, kFinishThreads, 0, ctx->stream>>>(make_reduce(ctx, dres, nb));
+  ctx->launches += 2;
   LBCU_CUDA(cudaGetLastError());
 }
 

@@ -125,9 +125,9 @@ __device__ __forceinline__ T ldg(const T* p) {
 
 // ---- deterministic reductions ---------------------------------------------
 // Each block reduces NR values (warp shuffles + shared memory) and writes its
-// partials to part[(offset + blockIdx) * NR + k]. The block that arrives last
-// on the ticket sums all partials in a fixed order and writes result[k], so
-// the value does not depend on block scheduling.
+// partials to part[(offset + blockIdx) * NR + k]; k_reduce_finish, launched
+// after the last contributing kernel, sums all partials in a fixed order and
+// writes result[k], so the value does not depend on block scheduling.
 // Device CG state (one per context, solver.cpp).
 struct CgState {
   double rr, rr_new, pap, alpha, beta, bnorm, tol, best, rel;
@@ -172,11 +172,10 @@ enum RedPost { POST_NONE = 0, POST_ALPHA = 1, POST_END = 2 };
 
 struct Reduce {
   double* part;        // partials, >= total_blocks * NR
-  unsigned* ticket;    // zero between reductions
   double* result;      // NR outputs
   int offset;          // this launch's first partial slot
   int total_blocks;    // partial slots over all launches that feed this result
-  // optional CG scalar step on result[0] by the finishing block
+  // optional CG scalar step on result[0] by k_reduce_finish
   int post;
   CgState* cg;
   double* hist;
@@ -184,12 +183,12 @@ struct Reduce {
   int use_graph;
 };
 
-// Split form for the hop kernels (measured: profiles/r03_cgvar*): each block
-// only writes its partial (no fence, no ticket, so it retires as soon as its
-// warps are done), and k_reduce_finish, launched after the last contributing
-// launch, sums the partials in a fixed order and runs the CG step. The
-// fence + atomic + second barrier of the last-block form kept every block's
-// registers idle for ~2 us and cost 20-29 us per 0.5 M-site eo hop.
+// Split form (measured: profiles/r03_cg_epilogue_breakdown.txt): each block
+// only writes its partial (no fence, no atomic ticket, so it retires as soon
+// as its warps are done), and k_reduce_finish sums the partials in a fixed
+// order and runs the CG step. The earlier last-block form (fence + atomic +
+// second barrier in every block) kept every block's registers idle for ~2 us
+// and cost 20-29 us per 0.5 M-site eo hop.
 template <int NR>
 __device__ __forceinline__ void block_reduce_partial(const Reduce& R, double (&v)[NR]) {
   __shared__ double sh[32][NR];
@@ -250,61 +249,6 @@ __global__ void __launch_bounds__(kFinishThreads) k_reduce_finish(const Reduce R
       for (int w = 0; w < kFinishThreads / 32; ++w) s += sh[w][k];
       R.result[k] = s;
     }
-    if (R.post == POST_ALPHA) cg_post_alpha(R.cg, R.result[0]);
-    else if (R.post == POST_END) cg_post_end(R.cg, R.result[0], R.hist, R.handle, R.use_graph);
-  }
-}
-
-template <int NR>
-__device__ __forceinline__ void block_reduce_finalize(const Reduce& R, double (&v)[NR]) {
-  __shared__ double sh[32][NR];
-  __shared__ bool last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarps = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int k = 0; k < NR; ++k)
-    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NR; ++k) sh[warp][k] = v[k];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s[NR];
-#pragma unroll
-    for (int k = 0; k < NR; ++k) {
-      s[k] = 0.0;
-      for (int w = 0; w < nwarps; ++w) s[k] += sh[w][k];
-      R.part[(size_t)(R.offset + blockIdx.x) * NR + k] = s[k];
-    }
-    __threadfence();
-    const unsigned t = atomicAdd(R.ticket, 1u);
-    last = (t == (unsigned)R.total_blocks - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double acc[NR];
-#pragma unroll
-  for (int k = 0; k < NR; ++k) acc[k] = 0.0;
-  for (int b = threadIdx.x; b < R.total_blocks; b += blockDim.x)
-#pragma unroll
-    for (int k = 0; k < NR; ++k) acc[k] += __ldcg(&R.part[(size_t)b * NR + k]);
-#pragma unroll
-  for (int k = 0; k < NR; ++k)
-    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], o);
-  __syncthreads();
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NR; ++k) sh[warp][k] = acc[k];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NR; ++k) {
-      double s = 0.0;
-      for (int w = 0; w < nwarps; ++w) s += sh[w][k];
-      R.result[k] = s;
-    }
-    *R.ticket = 0u;
     if (R.post == POST_ALPHA) cg_post_alpha(R.cg, R.result[0]);
     else if (R.post == POST_END) cg_post_end(R.cg, R.result[0], R.hist, R.handle, R.use_graph);
   }

@@ -742,7 +742,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     }
     if (reduce) {
       if (blocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
-      A.red = Reduce{ctx->partials, ctx->ticket, c.result, 0, blocks,
+      A.red = Reduce{ctx->partials, c.result, 0, blocks,
                      c.post, ctx->dcg, ctx->dhist, c.handle, c.use_graph};
     }
     // warp-shared z hops when every warp covers whole z-rows (hop_z_shared)
@@ -841,7 +841,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     int off = 0;
     for (int g2 = 0; g2 < gi; ++g2) off += int_blocks[g2] + bnd_blocks[g2];
     if (bnd) off += int_blocks[gi];
-    if (reduce) G.red = Reduce{ctx->partials, ctx->ticket, c.result, off, total_blocks};
+    if (reduce) G.red = Reduce{ctx->partials, c.result, off, total_blocks};
     return G;
   };
   // interior sites (no halo dependency) run on the compute stream while the
@@ -885,7 +885,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     ctx->launches += 1;
   }
   if (reduce) {  // all interior and boundary partials are in place
-    Reduce R{ctx->partials, ctx->ticket, c.result, 0, total_blocks};
+    Reduce R{ctx->partials, c.result, 0, total_blocks};
     k_reduce_finish<1><<<1, kFinishThreads, 0, s>>>(R);
     ctx->launches += 1;
   }

@@ -64,7 +64,6 @@ struct lbcu_ctx_s {
   // reduction workspace
   double* partials = nullptr;
   int max_partials = 0;
-  unsigned* ticket = nullptr;
   double* dscal = nullptr;  // 64 device scalars (reduction results)
   double* hscal = nullptr;  // pinned mirror
   // interior / boundary site lists per output parity (decomposed runs only)
