@@ -10,7 +10,10 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <type_traits>
+
 #include "links.cuh"
+
 #include "objects.hpp"
 
 namespace lbcu {
@@ -152,31 +155,53 @@ __device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a
 // Device order: per parity block, nv / ng groups (link: one per mu) of ng
 // elements per site, each group stride x ng elements in 32-site tiles (eidx).
 // A block stages TS consecutive sites (TS even -> TS/2 cb sites per parity).
+// Per (parity, cb) slot of the block's tile: the site's row in the staged
+// tile (local lexicographic s - s0), with bit 30 set when the antiperiodic
+// sign applies, or -1 past the end. Computed once per site, not per element.
+__device__ __forceinline__ void tile_rows(int* rows, long long s0, int half, long long vol, const DevGeo& g,
+                                          int sign_t, int t_off) {
+  for (int pj = threadIdx.x; pj < 2 * half; pj += blockDim.x) {
+    const int p = pj / half, jj = pj - p * half;
+    const long long cb = s0 / 2 + jj;
+    int row = -1;
+    if (2 * cb < vol) {
+      int c[4], s;
+      cb_coords(g, (int)cb, p, c, s);
+      row = static_cast<int>(s - s0) | ((c[0] + t_off == sign_t) ? (1 << 30) : 0);
+    }
+    rows[pj] = row;
+  }
+}
+
+// Host AoS (site-major records of nv entries) -> device tiled parity blocks.
+// The staged tile uses a row stride of nv + 1 entries, so the column reads of
+// the scatter phase (consecutive cb sites = every other row) hit distinct
+// shared-memory banks; stores are 32-site coalesced.
 template <class T>
 __global__ void k_aos_to_soa(const T* __restrict__ src, T* dst0, T* dst1, int nv, int ng, long long vol,
                              long long stride, int TS, DevGeo g, int sign_entries, int sign_t,
                              int t_off) {
   extern __shared__ unsigned char smraw[];
+  const int ld = nv + 1;
   T* sm = reinterpret_cast<T*>(smraw);
+  int* rows = reinterpret_cast<int*>(sm + (size_t)TS * ld);
   const long long s0 = (long long)blockIdx.x * TS;
+  const int half = TS / 2;
+  tile_rows(rows, s0, half, vol, g, sign_t, t_off);
   const int tile = TS * nv;
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-    const long long gi = s0 * nv + e;
-    if (s0 + e / nv < vol) sm[e] = src[gi];
+    const int site = e / nv, k = e - site * nv;
+    if (s0 + site < vol) sm[site * ld + k] = src[s0 * nv + e];
   }
   __syncthreads();
-  const int half = TS / 2;
   for (int e = threadIdx.x; e < 2 * nv * half; e += blockDim.x) {
-    const int jj = e % half, k = (e / half) % nv, p = e / (half * nv);
+    const int jj = e % half, pk = e / half, p = pk & 1, k = pk >> 1;
     T* dst = p ? dst1 : dst0;
-    if (!dst) continue;
-    const long long cb = s0 / 2 + jj;
-    if (2 * cb >= vol) continue;
-    int c[4], s;
-    cb_coords(g, (int)cb, p, c, s);
-    T v = sm[(s - s0) * nv + k];
-    if (k < sign_entries && c[0] + t_off == sign_t) v = neg(v);
-    dst[(k / ng) * ng * stride + eidx(ng, k % ng, cb)] = v;
+    const int row = rows[p * half + jj];
+    if (!dst || row < 0) continue;
+    T v = sm[(row & ((1 << 30) - 1)) * ld + k];
+    if (k < sign_entries && (row >> 30)) v = neg(v);
+    dst[(k / ng) * ng * stride + eidx(ng, k % ng, s0 / 2 + jj)] = v;
   }
 }
 
@@ -184,28 +209,83 @@ template <class T>
 __global__ void k_soa_to_aos(const T* src0, const T* src1, T* __restrict__ dst, int nv, int ng,
                              long long vol, long long stride, int TS, DevGeo g) {
   extern __shared__ unsigned char smraw[];
+  const int ld = nv + 1;
   T* sm = reinterpret_cast<T*>(smraw);
+  int* rows = reinterpret_cast<int*>(sm + (size_t)TS * ld);
   const long long s0 = (long long)blockIdx.x * TS;
   const int half = TS / 2;
+  tile_rows(rows, s0, half, vol, g, -1, 0);
+  __syncthreads();
   for (int e = threadIdx.x; e < 2 * nv * half; e += blockDim.x) {
-    const int jj = e % half, k = (e / half) % nv, p = e / (half * nv);
-    const long long cb = s0 / 2 + jj;
-    if (2 * cb >= vol) continue;
-    int c[4], s;
-    cb_coords(g, (int)cb, p, c, s);
+    const int jj = e % half, pk = e / half, p = pk & 1, k = pk >> 1;
+    const int row = rows[p * half + jj];
+    if (row < 0) continue;
     const T* src = p ? src1 : src0;
-    sm[(s - s0) * nv + k] = src ? src[(k / ng) * ng * stride + eidx(ng, k % ng, cb)] : T{};
+    sm[row * ld + k] = src ? src[(k / ng) * ng * stride + eidx(ng, k % ng, s0 / 2 + jj)] : T{};
   }
   __syncthreads();
   const int tile = TS * nv;
-  for (int e = threadIdx.x; e < tile; e += blockDim.x)
-    if (s0 + e / nv < vol) dst[s0 * nv + e] = sm[e];
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+    const int site = e / nv, k = e - site * nv;
+    if (s0 + site < vol) dst[s0 * nv + e] = sm[site * ld + k];
+  }
+}
+
+// Spinor fast path: NV = 4 dr entries per site known at compile time, one
+// group (ng = nv), 128 sites (2 device tiles per parity) per block, so every
+// index split is a shift or a constant division.
+template <int NV>
+constexpr int kSpTS = NV <= 16 ? 128 : 64;  // static shared memory <= 48 KB
+template <int NV>
+__global__ void __launch_bounds__(256) k_sp_to_soa(const double2* __restrict__ src, double2* dst0, double2* dst1,
+                                                   long long vol, DevGeo g) {
+  constexpr int TS = kSpTS<NV>, ld = NV + 1, half = TS / 2;
+  __shared__ double2 sm[TS * ld];
+  __shared__ int rows[TS];
+  const long long s0 = (long long)blockIdx.x * TS;
+  tile_rows(rows, s0, half, vol, g, -1, 0);
+  for (int e = threadIdx.x; e < TS * NV; e += blockDim.x) {
+    const int site = e / NV, k = e - site * NV;
+    if (s0 + site < vol) sm[site * ld + k] = src[s0 * NV + e];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * NV * half; e += blockDim.x) {
+    const int jj = e & (half - 1), pk = e / half, p = pk & 1, k = pk >> 1;
+    double2* dst = p ? dst1 : dst0;
+    const int row = rows[p * half + jj];
+    if (!dst || row < 0) continue;
+    dst[eidx(NV, k, s0 / 2 + jj)] = sm[row * ld + k];
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_sp_to_aos(const double2* src0, const double2* src1,
+                                                   double2* __restrict__ dst, long long vol, DevGeo g) {
+  constexpr int TS = kSpTS<NV>, ld = NV + 1, half = TS / 2;
+  __shared__ double2 sm[TS * ld];
+  __shared__ int rows[TS];
+  const long long s0 = (long long)blockIdx.x * TS;
+  tile_rows(rows, s0, half, vol, g, -1, 0);
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * NV * half; e += blockDim.x) {
+    const int jj = e & (half - 1), pk = e / half, p = pk & 1, k = pk >> 1;
+    const int row = rows[p * half + jj];
+    if (row < 0) continue;
+    const double2* src = p ? src1 : src0;
+    sm[row * ld + k] = src ? src[eidx(NV, k, s0 / 2 + jj)] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < TS * NV; e += blockDim.x) {
+    const int site = e / NV, k = e - site * NV;
+    if (s0 + site < vol) dst[s0 * NV + e] = sm[site * ld + k];
+  }
 }
 
 template <class T>
 int tile_sites(int nv) {
-  int ts = static_cast<int>((40 * 1024) / (nv * sizeof(T)));
-  ts = std::min(64, ts) & ~1;
+  // up to 256 sites (4 device tiles per parity) within ~40 KB of staging
+  int ts = static_cast<int>((40 * 1024) / ((nv + 1) * sizeof(T) + sizeof(int)));
+  ts = ts >= 64 ? std::min(256, ts) & ~63 : ts & ~1;
   return std::max(2, ts);
 }
 
@@ -308,12 +388,35 @@ void cg_scalar_end(lbcu_ctx_s* ctx, const double* rr_new, unsigned long long han
   LBCU_CUDA(cudaGetLastError());
 }
 
+template <class F>
+static bool spinor_fast(int nv, F&& f) {
+  switch (nv) {
+    case 8: f(std::integral_constant<int, 8>{}); return true;
+    case 12: f(std::integral_constant<int, 12>{}); return true;
+    case 16: f(std::integral_constant<int, 16>{}); return true;
+    case 24: f(std::integral_constant<int, 24>{}); return true;
+    default: return false;
+  }
+}
+
 template <class T>
 static void launch_to_soa(lbcu_ctx_s* ctx, const T* src, T* d0, T* d1, int nv, int sign_entries,
                           int ng = 0) {
   const Geometry& geo = ctx->geo;
+  if constexpr (std::is_same_v<T, double2>) {
+    if (sign_entries == 0 && (ng == 0 || ng == nv) &&
+        spinor_fast(nv, [&](auto Nc) {
+          constexpr int TS = kSpTS<decltype(Nc)::value>;
+          const int blocks = static_cast<int>((geo.volume + TS - 1) / TS);
+          k_sp_to_soa<decltype(Nc)::value><<<blocks, 256, 0, ctx->stream>>>(src, d0, d1, geo.volume, ctx->dgeo);
+        })) {
+      ctx->launches++;
+      LBCU_CUDA(cudaGetLastError());
+      return;
+    }
+  }
   const int TS = tile_sites<T>(nv);
-  const size_t smem = static_cast<size_t>(TS) * nv * sizeof(T);
+  const size_t smem = static_cast<size_t>(TS) * (nv + 1) * sizeof(T) + TS * sizeof(int);
   const int blocks = static_cast<int>((geo.volume + TS - 1) / TS);
   const int sign_t = sign_entries ? geo.global[0] - 1 : -1;
   const int t_off = geo.coords[0] * geo.local[0];
@@ -326,8 +429,19 @@ static void launch_to_soa(lbcu_ctx_s* ctx, const T* src, T* d0, T* d1, int nv, i
 template <class T>
 static void launch_to_aos(lbcu_ctx_s* ctx, const T* s0, const T* s1, T* dst, int nv, int ng = 0) {
   const Geometry& geo = ctx->geo;
+  if constexpr (std::is_same_v<T, double2>) {
+    if ((ng == 0 || ng == nv) && spinor_fast(nv, [&](auto Nc) {
+          constexpr int TS = kSpTS<decltype(Nc)::value>;
+          const int blocks = static_cast<int>((geo.volume + TS - 1) / TS);
+          k_sp_to_aos<decltype(Nc)::value><<<blocks, 256, 0, ctx->stream>>>(s0, s1, dst, geo.volume, ctx->dgeo);
+        })) {
+      ctx->launches++;
+      LBCU_CUDA(cudaGetLastError());
+      return;
+    }
+  }
   const int TS = tile_sites<T>(nv);
-  const size_t smem = static_cast<size_t>(TS) * nv * sizeof(T);
+  const size_t smem = static_cast<size_t>(TS) * (nv + 1) * sizeof(T) + TS * sizeof(int);
   const int blocks = static_cast<int>((geo.volume + TS - 1) / TS);
   k_soa_to_aos<T><<<blocks, 256, smem, ctx->stream>>>(s0, s1, dst, nv, ng ? ng : nv, geo.volume, geo.stride, TS,
                                                       ctx->dgeo);
