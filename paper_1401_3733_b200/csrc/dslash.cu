@@ -358,54 +358,25 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
 #pragma unroll
       for (int cc = 0; cc < D; ++cc) acc[k][cc] = make_double2(0.0, 0.0);
     const double2* in = A.in[par ^ 1];
-    // Direction order (profiles/r03_tune_order*): z y x t is 6 % faster for
-    // the full Dphi and 2-5 % for the eo hop with SU(2) links (fundamental and
-    // adjoint); t x y z stays best for R12 and AS4R. -DLBCU_HOP_ORDER=k
-    // forces one order for A/B builds (tools/build_variant.sh).
-#ifndef LBCU_HOP_ORDER
-#define LBCU_HOP_ORDER -1
+    // Direction order as a 4-digit code of mu values, first hop first
+    // (profiles/r03_tune_order*, r03_tune_perm*): the order changes how ptxas
+    // batches the loads. z y x t (3210) is 6 % faster for the full Dphi and
+    // 2-5 % for the eo hop with SU(2) links (fundamental and adjoint);
+    // t x y z (0123) stays best for R12 and AS4R. -DLBCU_HOP_PERM=dddd forces
+    // one order for A/B builds (tools/build_variant.sh).
+#ifndef LBCU_HOP_PERM
+#define LBCU_HOP_PERM -1
 #endif
-    constexpr int kOrder = LBCU_HOP_ORDER >= 0 ? LBCU_HOP_ORDER : (FMT == GF_SU2 || (D == 2 && !REAL)) ? 1 : 0;
-    auto z_hop = [&] {
-      if constexpr (ZS) hop_z_shared<D, REAL, FMT>(acc, A, in, par, i, s, mask);
-      else hop_mu<D, REAL, FMT, BND, 3>(acc, A, in, par, i, s, c);
+    constexpr int kPerm = LBCU_HOP_PERM >= 0 ? LBCU_HOP_PERM : (FMT == GF_SU2 || (D == 2 && !REAL)) ? 3210 : 123;
+    auto dir = [&](auto Mc) {
+      constexpr int MU = decltype(Mc)::value;
+      if constexpr (MU == 3 && ZS) hop_z_shared<D, REAL, FMT>(acc, A, in, par, i, s, mask);
+      else hop_mu<D, REAL, FMT, BND, MU>(acc, A, in, par, i, s, c);
     };
-    if constexpr (kOrder == 1) {  // z y x t
-      z_hop();
-      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
-    } else if constexpr (kOrder == 5) {  // y z x t
-      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-      z_hop();
-      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
-    } else if constexpr (kOrder == 6) {  // z y t x
-      z_hop();
-      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
-    } else if constexpr (kOrder == 7) {  // z x y t
-      z_hop();
-      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
-    } else if constexpr (kOrder == 2) {  // t z x y
-      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
-      z_hop();
-      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-    } else if constexpr (kOrder == 3) {  // x t y z
-      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-      z_hop();
-    } else {  // t x y z
-      hop_mu<D, REAL, FMT, BND, 0>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 1>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, BND, 2>(acc, A, in, par, i, s, c);
-      z_hop();
-    }
+    dir(std::integral_constant<int, kPerm / 1000>{});
+    dir(std::integral_constant<int, kPerm / 100 % 10>{});
+    dir(std::integral_constant<int, kPerm / 10 % 10>{});
+    dir(std::integral_constant<int, kPerm % 10>{});
     if constexpr (FMT == GF_AS4R) {  // back from the real-basis colour frame
 #pragma unroll
       for (int sp = 0; sp < 4; ++sp) as4r_out(acc[sp], 0.5);
