@@ -386,6 +386,155 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
   }
 }
 
+// ---- experiment: TMA-staged row blocks (full Dphi, SU(2) links, Lz = 32) ----
+// A block of 8 warps owns 8 consecutive y-rows of one (t, x) plane, both
+// parities (warps 0-3 parity 0, 4-7 parity 1; a warp = one 32-site tile = 2
+// rows). Thread 0 stages, with 12 bulk copies (cp.async.bulk, one 4 KB tile
+// each, completion on an mbarrier), the input tiles of rows y0-2 .. y0+9 of
+// both parities: every y, z and diagonal operand of the block. While they
+// travel, each thread does its t and x hops from global memory; then the y
+// and z hops and the diagonal term read shared memory.
+constexpr int kRbRows = 8, kRbTiles = (kRbRows + 4) / 2;  // tiles per parity
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <int D, int P0, int P1, int F0, int F1>
+__device__ __forceinline__ void project_sm(double2 (&h)[2][D], const double2* q, double s5) {
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const double2 a0 = q[(0 * D + c) * kTile], a1 = q[(1 * D + c) * kTile];
+    const double2 b0 = q[(P0 * D + c) * kTile], b1 = q[(P1 * D + c) * kTile];
+    h[0][c] = cadd(a0, phm<F0>(cscale(s5, b0)));
+    h[1][c] = cadd(a1, phm<F1>(cscale(s5, b1)));
+  }
+}
+
+template <int D, bool REAL, int FMT, int MINB>
+__global__ void __launch_bounds__(256, MINB) hop_rowblock_kernel(const __grid_constant__ HopArgs A) {
+  extern __shared__ __align__(128) unsigned char rb_raw[];
+  constexpr int TILE = 4 * D * kTile;                 // double2 per tile
+  constexpr int STAGE = 2 * kRbTiles * TILE;          // double2 per stage
+  double2* sm0 = reinterpret_cast<double2*>(rb_raw);  // [stage][parity][kRbTiles][4D][32]
+  __shared__ __align__(8) unsigned long long bar[2];
+  const int Ly = A.g.L[2];
+  const int nyb = Ly / kRbRows;
+  const int nblk = A.g.L[0] * A.g.L[1] * nyb;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int par = w >> 2, pairk = w & 3;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar[k])), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  auto issue = [&](int blk, int stage) {
+    const int yb = blk % nyb, tx = blk / nyb, y0 = yb * kRbRows;
+    const unsigned bytes = STAGE * sizeof(double2);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[stage])), "r"(bytes)
+                 : "memory");
+    for (int pp = 0; pp < 2; ++pp)
+      for (int k = 0; k < kRbTiles; ++k) {
+        const int y = (y0 - 2 + 2 * k + Ly) % Ly;
+        const double2* src = A.in[pp] + (long long)((tx * Ly + y) >> 1) * TILE;
+        double2* dst = sm0 + stage * STAGE + (pp * kRbTiles + k) * TILE;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(dst)),
+            "l"(src), "r"((unsigned)(TILE * sizeof(double2))), "r"(smem_u32(&bar[stage]))
+            : "memory");
+      }
+  };
+  if (threadIdx.x == 0 && blockIdx.x < nblk) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+    const int stage = it & 1;
+    // prefetch the next block into the other stage (its previous contents
+    // were consumed before the __syncthreads at the end of the last iteration)
+    if (threadIdx.x == 0 && blk + gridDim.x < nblk) issue(blk + gridDim.x, stage ^ 1);
+    double2* sm = sm0 + stage * STAGE;
+    const int yb = blk % nyb, tx = blk / nyb, y0 = yb * kRbRows;
+    auto tile_of = [&](int y) { return (tx * Ly + y) >> 1; };
+  // this thread's output site
+  const int i = tile_of(y0 + 2 * pairk) * 32 + lane;  // cb index in parity `par`
+  int c[4], s;
+  cb_coords(A.g, i, par, c, s);
+  double2 acc[4][D];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) acc[k][cc] = make_double2(0.0, 0.0);
+  const double2* in = A.in[par ^ 1];
+  hop_mu<D, REAL, FMT, false, 1>(acc, A, in, par, i, s, c);
+  hop_mu<D, REAL, FMT, false, 0>(acc, A, in, par, i, s, c);
+  // wait for the staged tiles of this stage (phase flips every second block)
+  {
+    unsigned done = 0;
+    const unsigned phase = (it >> 1) & 1;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(smem_u32(&bar[stage])), "r"(phase)
+          : "memory");
+  }
+  const long long st = A.g.stride;
+  const int q = par ^ 1;
+  // staged-tile address of the input site (row y, cb within row) of parity pp
+  auto sm_site = [&](int pp, int y, int cbrow) -> const double2* {
+    int k = ((y - (y0 - 2) + Ly) % Ly) >> 1;  // row pair slot
+    const int r = y & 1;
+    return sm + (pp * kRbTiles + k) * TILE + r * 16 + cbrow;
+  };
+  const int hz = A.g.L[3] >> 1;  // 16
+  const int cbrow = i % hz;        // position of the output cb within its row
+  const int dz = s & 1, yy = c[2];
+#pragma unroll
+  for (int dir = 0; dir < 2; ++dir) {
+    using G = Gam<2>;
+    // y hops: neighbour rows y +- 1, same cb position within the row
+    double2 h[2][D];
+    const int yn = dir == 0 ? (yy + 1) % Ly : (yy - 1 + Ly) % Ly;
+    if (dir == 0) {
+      project_sm<D, G::p0, G::p1, G::f0, G::f1>(h, sm_site(q, yn, cbrow), A.s5in);
+      link_hop<D, REAL, FMT, false, G::r0, G::r1, G::q0, G::q1>(acc, link_ptr<D, REAL, FMT>(A.gauge, st, par, 2, i), st, h);
+    } else {
+      project_sm<D, G::p0, G::p1, G::f0 ^ 1, G::f1 ^ 1>(h, sm_site(q, yn, cbrow), A.s5in);
+      const int nb = nb_bwd(A.g, s, c, 2) >> 1;
+      link_hop<D, REAL, FMT, true, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, link_ptr<D, REAL, FMT>(A.gauge, st, q, 2, nb), st, h);
+    }
+  }
+  {
+    using G = Gam<3>;
+    // z hops: own row; z+ at cb position (dz == 0 ? same : +1), z- at (dz == 0 ? -1 : same), row-periodic
+    const int cp = dz == 0 ? cbrow : (cbrow + 1) % hz;
+    const int cm = dz == 0 ? (cbrow - 1 + hz) % hz : cbrow;
+    double2 h[2][D];
+    project_sm<D, G::p0, G::p1, G::f0, G::f1>(h, sm_site(q, yy, cp), A.s5in);
+    link_hop<D, REAL, FMT, false, G::r0, G::r1, G::q0, G::q1>(acc, link_ptr<D, REAL, FMT>(A.gauge, st, par, 3, i), st, h);
+    project_sm<D, G::p0, G::p1, G::f0 ^ 1, G::f1 ^ 1>(h, sm_site(q, yy, cm), A.s5in);
+    const int nb = nb_bwd(A.g, s, c, 3) >> 1;
+    link_hop<D, REAL, FMT, true, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, link_ptr<D, REAL, FMT>(A.gauge, st, q, 3, nb), st, h);
+  }
+  // epilogue: out = a x + b acc with x = in (full Dphi), x from shared memory
+  const double2* xs = sm_site(par, yy, cbrow);
+  double2* __restrict__ out = site_ptr<4 * D>(A.out[par], i);
+#pragma unroll
+  for (int sp = 0; sp < 4; ++sp)
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) {
+      const double bs = sp < 2 ? A.b : A.b * A.s5acc;
+      const double as = sp < 2 ? A.a : A.a * A.s5x;
+      const double2 xv = xs[(sp * D + cc) * kTile];
+      double2 v = cscale(bs, acc[sp][cc]);
+      v.x = fma(as, xv.x, v.x);
+      v.y = fma(as, xv.y, v.y);
+      out[(sp * D + cc) * kTile] = v;
+    }
+  __syncthreads();  // every warp is done with this stage before it is refilled
+  }
+}
+
 // out = a x + b acc (gamma5 signs folded), then store / store + |out|^2 /
 // CG residual update. Two phases: every load (x, r) is issued before any
 // store, and the pointers are restrict-qualified, so the 4 dr round trips
@@ -715,6 +864,23 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       if (blocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
       A.red = Reduce{ctx->partials, c.result, 0, blocks,
                      c.post, ctx->dcg, ctx->dhist, c.handle, c.use_graph};
+    }
+    // experiment (off by default, 8 % slower: profiles/r03_tune_rb*_cfg2.log):
+    // TMA-staged row blocks for the full Dphi with SU(2) links
+    if (env_int("LBCU_HOP_RB", 0) && npar == 2 && c.epi == EPI_STORE && c.x == c.in && fmt == GF_SU2 &&
+        dr == 2 && !real && geo.local[3] == 32 && geo.local[2] % kRbRows == 0) {
+      const int nb = std::min(geo.local[0] * geo.local[1] * (geo.local[2] / kRbRows), 148 * 2);
+      const size_t smem = 2ull * 2ull * kRbTiles * 4 * dr * kTile * sizeof(double2);
+      static bool attr = false;
+      if (!attr) {
+        LBCU_CUDA(cudaFuncSetAttribute(hop_rowblock_kernel<2, false, GF_SU2, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+      }
+      hop_rowblock_kernel<2, false, GF_SU2, 2><<<nb, 256, smem, s>>>(A);
+      ctx->launches += 1;
+      LBCU_CUDA(cudaGetLastError());
+      return;
     }
     // warp-shared z hops when every warp covers whole z-rows (hop_z_shared)
     const int hz = geo.local[3] / 2;

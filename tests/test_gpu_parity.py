@@ -375,3 +375,18 @@ def test_direct_halo_toggle_matches():
 
     for res in run_ranks(4, body):
         assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
+
+
+def test_tma_rowblock_dphi_matches_oracle(monkeypatch):
+    """The TMA-staged row-block full Dphi (experiment, LBCU_HOP_RB=1; DESIGN
+    §4: correct but 8 % slower than the default kernel): persistent blocks,
+    cp.async.bulk tiles completed on an mbarrier, double-buffered."""
+    monkeypatch.setenv("LBCU_HOP_RB", "1")
+    L = [4, 6, 16, 32]
+    dr, g, s = fields(L, 2, lb.FUNDAMENTAL)
+    ctx = lb.Context(L)
+    gauge = lb.GaugeField(ctx, 2, lb.FUNDAMENTAL, lb.ANTIPERIODIC_T).upload(g)
+    a, b = lb.SpinorField(ctx, dr).upload(s), lb.SpinorField(ctx, dr)
+    lb.apply_dirac(b, gauge, a, 0.1)
+    assert gauge.storage()[0] == "su2"
+    assert rel_l2(b.download(), O.port_dirac(L, 1, 0.1, g, s)) < 1e-13
