@@ -320,6 +320,10 @@ int lbcu_ctx_create(lbcu_world w, int rank, int device, const int global[4], con
       }
       ctx->nint[p] = static_cast<int>(in.size());
       ctx->nbnd[p] = static_cast<int>(bd.size());
+      // a run of consecutive cb indices (only T decomposed): the interior
+      // launch then indexes directly (no list load, warp-shared z hops)
+      ctx->int_lo[p] = -1;
+      if (!in.empty() && in.back() - in.front() + 1 == static_cast<int>(in.size())) ctx->int_lo[p] = in.front();
       LBCU_CUDA(cudaMalloc(&ctx->ilist[p], sizeof(int) * std::max<size_t>(1, in.size())));
       LBCU_CUDA(cudaMalloc(&ctx->blist[p], sizeof(int) * std::max<size_t>(1, bd.size())));
       if (!in.empty())

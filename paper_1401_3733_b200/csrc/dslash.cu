@@ -61,6 +61,7 @@ struct HopArgs {
   // and all 8 uses of every spinor then fall within ~2 slices of one block,
   // a window sized to stay in L2 (hop_apply).
   int sched_len, sched_cpb, sched_bx;
+  int ioff[2];  // cb offset of a list-free partial launch (contiguous interior)
   Reduce red;
 };
 
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ 
 template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS>
 __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1], unsigned mask) {
   {
-    const int i = A.list[par] ? A.list[par][idx] : idx;
+    const int i = A.list[par] ? A.list[par][idx] : idx + A.ioff[par];
     int c[4], s;
     cb_coords(A.g, i, par, c, s);
     double2 acc[4][D];
@@ -974,7 +975,11 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     G.both = joint ? 1 : 0;
     G.par0 = p;
     G.nsites = bnd ? ctx->nbnd[p] : ctx->nint[p];
-    for (int pp = 0; pp < 2; ++pp) G.list[pp] = bnd ? ctx->blist[pp] : ctx->ilist[pp];
+    for (int pp = 0; pp < 2; ++pp) {
+      const bool run = !bnd && ctx->int_lo[pp] >= 0;
+      G.list[pp] = run ? nullptr : bnd ? ctx->blist[pp] : ctx->ilist[pp];
+      G.ioff[pp] = run ? ctx->int_lo[pp] : 0;
+    }
     int off = 0;
     for (int g2 = 0; g2 < gi; ++g2) off += int_blocks[g2] + bnd_blocks[g2];
     if (bnd) off += int_blocks[gi];
@@ -987,10 +992,15 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   // event that the peers' streams wait on before their boundary launch.
   if (direct) T->post(ctx->rank, epoch, s);
   else LBCU_CUDA(cudaEventRecord(ctx->ev_pack, s));
+  // warp-shared z hops for a contiguous interior whose warps cover whole z-rows
+  const int hz = geo.local[3] / 2;
   for (int gi = 0; gi < ngroups; ++gi) {
     HopArgs Ai = group_args(gi, false);
+    const bool zs = env_int("LBCU_HOP_ZS", 1) && !geo.decomposed[3] && hz > 0 && 32 % hz == 0 &&
+                    ctx->int_lo[0] >= 0 && ctx->int_lo[1] >= 0 && ctx->int_lo[0] % 32 == 0 &&
+                    ctx->int_lo[1] % 32 == 0;
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ai, false, c.epi, Ai.nsites, joint ? 2 : 1, s);
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(Ai, false, c.epi, Ai.nsites, joint ? 2 : 1, s, 0, zs);
     });
     ctx->launches += 1;
   }

@@ -70,6 +70,7 @@ struct lbcu_ctx_s {
   int* ilist[2] = {nullptr, nullptr};
   int* blist[2] = {nullptr, nullptr};
   int nint[2] = {0, 0}, nbnd[2] = {0, 0};
+  int int_lo[2] = {-1, -1};  // first cb of a contiguous interior, -1: use ilist
   std::map<int, lbcu::HaloBufs> halo;  // keyed by dr
   std::map<std::tuple<int, int, int>, lbcu_spinor_s*> scratch;  // (dr, subset, slot)
   lbcu::CgState* dcg = nullptr;

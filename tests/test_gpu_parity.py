@@ -214,7 +214,7 @@ def test_tampered_operator_fails_consistency():
 
 @pytest.mark.parametrize("direct", [False, True], ids=["copy", "direct"])
 @pytest.mark.parametrize("grid", [(2, 1, 1, 1), (2, 1, 1, 2), (1, 2, 2, 1)], ids=["t2", "t2z2", "x2y2"])
-@pytest.mark.parametrize("n,rep", [REPS[0], REPS[3]], ids=[REP_IDS[0], REP_IDS[3]])
+@pytest.mark.parametrize("n,rep", [REPS[0], REPS[1], REPS[3]], ids=[REP_IDS[0], REP_IDS[1], REP_IDS[3]])
 def test_decomposed_dphi_matches_single(grid, n, rep, direct):
     """Serial oracle vs decomposition: ranks as host threads on one GPU,
     half-spinor halos packed by kernels and exchanged by the thread transport
