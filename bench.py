@@ -215,7 +215,7 @@ def run_reference(args, cfg):
     L, n, rep = cfg["L"], cfg["n"], cfg["rep"]
     dr = O.rep_dim(rep, n)
     nthreads = os.cpu_count() or 1
-    grid = O.grid_for_threads(L, nthreads)
+    grid = O.grid_for_threads_balanced(L, nthreads)
     cores = int(np.prod(grid))
     fps = O.ref_flops_per_site(O.DIRAC, dr, O.rep_is_real(rep))
     V = int(np.prod(L))
@@ -414,7 +414,7 @@ def run_gpu(args, cfg):
         try:
             import oracle as O
             nthreads = os.cpu_count() or 1
-            cgrid = O.grid_for_threads(L, nthreads)
+            cgrid = O.grid_for_threads_balanced(L, nthreads)
             one = O.ref_bench_dirac(L, cgrid, n, rep, mass, 1, 1)
             napps = int(max(1, min(200, args.cpu_seconds / max(one, 1e-6))))
             secs = O.ref_bench_dirac(L, cgrid, n, rep, mass, 1, napps)
