@@ -390,3 +390,24 @@ def test_tma_rowblock_dphi_matches_oracle(monkeypatch):
     lb.apply_dirac(b, gauge, a, 0.1)
     assert gauge.storage()[0] == "su2"
     assert rel_l2(b.download(), O.port_dirac(L, 1, 0.1, g, s)) < 1e-13
+
+
+EXTRA_REPS = [(3, lb.SYMMETRIC), (4, lb.FUNDAMENTAL), (3, lb.ADJOINT), (4, lb.SYMMETRIC), (6, lb.FUNDAMENTAL)]
+
+
+@pytest.mark.parametrize("n,rep", EXTRA_REPS, ids=["su3s", "su4f", "su3a", "su4s", "su6f"])
+def test_other_representations_match_oracle(n, rep):
+    """Every other device specialisation (dense links: dr 4, 6, 8 real, 10):
+    Dphi and Mhat against the oracle, eo CG against the reference-composed
+    solver."""
+    L = [4, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, n, rep)
+    out = lb.SpinorField(ctx, dr)
+    lb.apply_dirac(out, gauge, lb.SpinorField(ctx, dr).upload(s), 0.1)
+    assert rel_l2(out.download(), O.port_dirac(L, 1, 0.1, g, s)) < TOL_DPHI
+    me = lb.SpinorField(ctx, dr, lb.EVEN)
+    lb.mhat(me, gauge, lb.SpinorField(ctx, dr, lb.EVEN).upload(s), 0.1)
+    assert rel_l2(me.download(), O.port_mhat(L, 1, 0.1, g, s)) < TOL_DPHI
+    o = lb.cg_solve_eo(gauge, 0.1, lb.SpinorField(ctx, dr, lb.EVEN).upload(s), lb.CgSettings(1e-10, 1000))
+    ref = O.ref_cg_eo(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s, 1e-10)
+    assert abs(o.iterations - ref["iterations"]) <= 1 and o.true_rel_residual < 2e-10
