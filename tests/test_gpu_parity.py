@@ -411,3 +411,27 @@ def test_other_representations_match_oracle(n, rep):
     o = lb.cg_solve_eo(gauge, 0.1, lb.SpinorField(ctx, dr, lb.EVEN).upload(s), lb.CgSettings(1e-10, 1000))
     ref = O.ref_cg_eo(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s, 1e-10)
     assert abs(o.iterations - ref["iterations"]) <= 1 and o.true_rel_residual < 2e-10
+
+
+@pytest.mark.parametrize("n,rep", EXTRA_REPS, ids=["su3s", "su4f", "su3a", "su4s", "su6f"])
+def test_other_representations_decomposed(n, rep):
+    """Halo pack (dense links of every size, real and complex) and boundary
+    kernels for the remaining specialisations: 2x1x1x2 thread ranks with
+    direct halos against the serial oracle."""
+    L, grid = [8, 4, 4, 8], (2, 1, 1, 2)
+    dr, g, s = fields(L, n, rep)
+    want = O.port_dirac(L, 1, 0.1, g, s)
+    world = lb.World.threads(4, direct=True)
+
+    def body(r):
+        ctx = lb.Context(L, grid, r, 0, world)
+        idx = global_index(L, grid, r)
+        gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g[idx])
+        out = lb.SpinorField(ctx, dr)
+        lb.apply_dirac(out, gauge, lb.SpinorField(ctx, dr).upload(s[idx]), 0.1)
+        return idx, out.download()
+
+    got = np.empty_like(want)
+    for idx, part in run_ranks(4, body):
+        got[idx] = part
+    assert rel_l2(got, want) < 1e-14
