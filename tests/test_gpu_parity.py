@@ -435,3 +435,16 @@ def test_other_representations_decomposed(n, rep):
     for idx, part in run_ranks(4, body):
         got[idx] = part
     assert rel_l2(got, want) < 1e-14
+
+
+def test_dphi_host_pipeline_distinct_fields():
+    """lbcu_dphi_host over 5 distinct host fields (two device slots reused
+    through the copy/compute pipeline): every output is the Dphi of its own
+    input (reference layout both ways)."""
+    L, n, rep, m = [4, 4, 4, 8], 2, lb.FUNDAMENTAL, 0.1
+    ctx, dr, g, s, gauge = setup(L, n, rep)
+    ins = [np.ascontiguousarray(lb.init_spinor_random(L, dr, 1, k)) for k in range(5)]
+    outs = [np.zeros_like(x) for x in ins]
+    lb.dphi_host(gauge, m, [x.ctypes.data for x in ins], [y.ctypes.data for y in outs])
+    for x, y in zip(ins, outs):
+        assert rel_l2(y, O.port_dirac(L, 1, m, g, x)) < TOL_DPHI
