@@ -98,9 +98,10 @@ def bytes_eo_cg_iter(dr, real, fmt="full"):  # per even site 4
 
 
 def duplex_copy_ms(hin, hout, nbytes, reps=10):
-    """The bound of the e2e number: one pinned H2D and one pinned D2H of a
-    step's bytes running concurrently on two streams (plain cudaMemcpyAsync
-    through cuda-python; tools/pcie_probe.cu measures the same), ms per step."""
+    """The bound of the e2e number: pinned H2D and D2H copies of a step's
+    bytes, alone and running concurrently on two streams (plain
+    cudaMemcpyAsync through cuda-python; tools/pcie_probe.cu measures the
+    same), best of 3 passes, ms per step: {"both", "h2d", "d2h"}."""
     try:
         import torch
         from cuda.bindings import runtime as rt
@@ -110,24 +111,25 @@ def duplex_copy_ms(hin, hout, nbytes, reps=10):
     sh, sd = torch.cuda.Stream(), torch.cuda.Stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h2d, d2h = rt.cudaMemcpyKind.cudaMemcpyHostToDevice, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost
-    best = None
-    for _ in range(3):  # first pass warms the copy path; best of the rest
+
+    def run(mode):
         torch.cuda.synchronize()
         t0.record()
         sh.wait_event(t0)
         sd.wait_event(t0)
         for k in range(reps):
-            rt.cudaMemcpyAsync(dbuf[0].data_ptr(), hin[k % 2].data_ptr(), nbytes, h2d, sh.cuda_stream)
-            rt.cudaMemcpyAsync(hout[k % 2].data_ptr(), dbuf[1].data_ptr(), nbytes, d2h, sd.cuda_stream)
+            if mode != "d2h":
+                rt.cudaMemcpyAsync(dbuf[0].data_ptr(), hin[k % 2].data_ptr(), nbytes, h2d, sh.cuda_stream)
+            if mode != "h2d":
+                rt.cudaMemcpyAsync(hout[k % 2].data_ptr(), dbuf[1].data_ptr(), nbytes, d2h, sd.cuda_stream)
         cur = torch.cuda.current_stream()
         cur.wait_stream(sh)
         cur.wait_stream(sd)
         t1.record()
         torch.cuda.synchronize()
-        ms = t0.elapsed_time(t1) / reps
-        best = ms if best is None else min(best, ms)
-    return best
+        return t0.elapsed_time(t1) / reps
 
+    return {mode: min(run(mode) for _ in range(3)) for mode in ("both", "h2d", "d2h")}
 
 class ClockSampler:
     """NVML SM-clock / throttle-reason sampler run DURING the timed region."""
@@ -453,10 +455,13 @@ def run_gpu(args, cfg):
                     "d2h_bytes_per_step": nbytes, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
                     "api": "lbcu_dphi_host (pinned host buffers, reference layout)",
                     "check_rel_err": e2e_err,
-                    "pcie_bound": {"duplex_copy_ms_per_step": duplex_ms,
-                                   "frac": duplex_ms / (e2e_ms / e2e_steps) if duplex_ms else None,
-                                   "note": "concurrent pinned H2D + D2H of one step's bytes; "
-                                           "frac = that time / e2e ms per step"}},
+                    "pcie_bound": {"duplex_copy_ms_per_step": duplex_ms and duplex_ms["both"],
+                                   "h2d_copy_ms_per_step": duplex_ms and duplex_ms["h2d"],
+                                   "d2h_copy_ms_per_step": duplex_ms and duplex_ms["d2h"],
+                                   "frac": duplex_ms["both"] / (e2e_ms / e2e_steps) if duplex_ms else None,
+                                   "note": "pinned copies of one step's bytes, concurrent H2D + D2H (duplex, "
+                                           "±4 % run to run) and each direction alone (the floor); "
+                                           "frac = duplex time / e2e ms per step"}},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cg": cg,
