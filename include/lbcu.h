@@ -142,6 +142,10 @@ int lbcu_barrier(lbcu_ctx c);      /* Worker::barrier, transport.cpp:79 */
 int lbcu_allreduce_sum(lbcu_ctx c, double* values, int n);
 /* launches of library kernels issued on this context since creation */
 long long lbcu_ctx_kernel_launches(lbcu_ctx c);
+/* Instantiated CG solve graphs cached by the context (one per fused problem
+ * and field set; dropped when a field they name is destroyed or its links are
+ * re-uploaded, all of them at lbcu_ctx_destroy). -1 for a null context. */
+long long lbcu_ctx_cached_solves(lbcu_ctx c);
 /* CUDA-event timing on the context stream (slot 0..15) */
 int lbcu_event_record(lbcu_ctx c, int slot);
 int lbcu_event_elapsed_ms(lbcu_ctx c, int slot_a, int slot_b, float* ms);

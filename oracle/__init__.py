@@ -8,7 +8,9 @@ Two libraries, both built by ``oracle/Makefile`` into ``oracle/_ref/``:
 
 * ``liblatbench_ref.so`` — the UNMODIFIED reference (``/root/reference/proj``,
   compiled from its own sources) plus ``ref_shim.cpp``. Functions prefixed
-  ``ref_``.
+  ``ref_``. ``liblatbench_ref_v4.so`` is the same build for x86-64-v4
+  (AVX-512), loaded instead on hosts that support it (``LBCU_REF_ISA=v3``
+  forces the AVX2 build).
 * ``liboracle.so`` — ``oracle.c``, the plain-C restatement, pinned against the
   reference by ``tests/test_oracle.py``. Functions prefixed ``port_``.
 
@@ -28,6 +30,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REF_DIR = os.path.join(HERE, "_ref")
 REF_SO = os.path.join(REF_DIR, "liblatbench_ref.so")
 REF_EXACT_SO = os.path.join(REF_DIR, "liblatbench_ref_exact.so")
+REF_V4_SO = os.path.join(REF_DIR, "liblatbench_ref_v4.so")
 PORT_SO = os.path.join(REF_DIR, "liboracle.so")
 
 FUNDAMENTAL, ADJOINT, SYMMETRIC, ANTISYMMETRIC = 0, 1, 2, 3
@@ -48,6 +51,8 @@ def build(quiet: bool = True) -> None:
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/src"):
         targets.append("ref")
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1401_3733_b200", "liblbcu.so")):
+            targets.append("dropin")
     subprocess.run(["make", "-C", HERE, *targets], check=True,
                    stdout=subprocess.DEVNULL if quiet else None)
 
@@ -70,9 +75,54 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(_dp)
 
 
+def cpu_flags() -> set:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def host_cpu():
+    """lscpu-style facts of this host: model name, logical CPUs usable by this
+    process, physical cores (unique (package, core) pairs), ISA level of the
+    reference build that ref_lib() loads."""
+    model, cores, pkg = None, set(), None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                k, _, v = line.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "model name" and model is None:
+                    model = v
+                elif k == "physical id":
+                    pkg = v
+                elif k == "core id":
+                    cores.add((pkg, v))
+    except OSError:
+        pass
+    try:
+        logical = len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        logical = os.cpu_count() or 1
+    return {"model": model, "logical_cpus": logical, "physical_cores": len(cores) or None,
+            "reference_isa": ref_isa()}
+
+
+def ref_isa() -> str:
+    v4 = {"avx512f", "avx512bw", "avx512dq", "avx512vl"}
+    if os.environ.get("LBCU_REF_ISA") != "v3" and os.path.exists(REF_V4_SO) and v4 <= cpu_flags():
+        return "x86-64-v4"
+    return "x86-64-v3"
+
+
 def ref_lib():
-    """The compiled reference; the FMA-free build inside ``exact_reference()``."""
-    path = REF_EXACT_SO if _exact else REF_SO
+    """The compiled reference (the highest ISA build the host supports); the
+    FMA-free build inside ``exact_reference()``."""
+    path = REF_EXACT_SO if _exact else (REF_V4_SO if ref_isa() == "x86-64-v4" else REF_SO)
     lib = _refs.get(path)
     if lib is None:
         if not os.path.exists(path):
@@ -241,11 +291,49 @@ def ref_counted_dirac(L, n, rep):
     return v.value
 
 
-def ref_bench_dirac(L, grid, n, rep, mass, seed, napps):
-    secs = C.c_double()
-    _chk(ref_lib().ref_bench_dirac(_arr4(L), _arr4(grid), n, rep, C.c_double(mass), C.c_uint64(seed),
-                                   int(napps), C.byref(secs)))
-    return secs.value
+LINKS_HAAR, LINKS_NEAR_UNIT = 0, 1
+
+
+def ref_bench_dirac(L, grid, n, rep, mass, seed, napps, links=LINKS_HAAR, bc_time=1, eps=0.3, nwarm=1,
+                    nsamples=1):
+    """Seconds for `napps` reference apply_dirac on the BASELINE workload
+    (inputs generated per worker: Haar or near-unit links, antiperiodic t),
+    after `nwarm` untimed applications; a list when nsamples > 1."""
+    secs = (C.c_double * max(1, nsamples))()
+    _chk(ref_lib().ref_bench_dirac(_arr4(L), _arr4(grid), n, rep, int(links), C.c_double(eps), int(bc_time),
+                                   C.c_double(mass), C.c_uint64(seed), int(nwarm), int(napps), int(nsamples),
+                                   secs))
+    return list(secs) if nsamples > 1 else secs[0]
+
+
+def ref_cg_probe(L, grid, n, rep, mass, seed, eo, max_iterations, tol=0.0, links=LINKS_HAAR, bc_time=1,
+                 eps=0.3):
+    """The reference cg_solve on the BASELINE workload (plain on H, or the
+    composed eo operator), inputs generated per worker. tol > 0: a solve;
+    tol = 0: a bounded sample of exactly max_iterations iterations (plus a
+    1-iteration calibration call). Returns dict(seconds, iterations,
+    true_rel_residual, seconds_per_iteration), wall times."""
+    secs, its, trel, per = C.c_double(), C.c_long(), C.c_double(), C.c_double()
+    _chk(ref_lib().ref_cg_probe(_arr4(L), _arr4(grid), n, rep, int(links), C.c_double(eps), int(bc_time),
+                                C.c_double(mass), C.c_uint64(seed), int(bool(eo)), C.c_double(tol),
+                                int(max_iterations), C.byref(secs), C.byref(its), C.byref(trel), C.byref(per)))
+    return dict(seconds=secs.value, iterations=its.value, true_rel_residual=trel.value,
+                seconds_per_iteration=per.value)
+
+
+def ref_report_reformat(text: str, fmt: str = "json") -> str:
+    """Parse a format-1 JSON report with the reference's report_from_json and
+    re-emit it with its format_report (report.cpp:152-217)."""
+    lib = ref_lib()
+    if not hasattr(lib, "ref_report_reformat"):
+        raise RuntimeError("reference built without report.cpp (nlohmann json.hpp not found)")
+    code = {"text": 0, "json": 1, "csv": 2}[fmt]
+    n = C.c_size_t()
+    data = text.encode()
+    _chk(lib.ref_report_reformat(data, code, None, C.c_size_t(0), C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _chk(lib.ref_report_reformat(data, code, buf, C.c_size_t(n.value + 1), C.byref(n)))
+    return buf.value.decode()
 
 
 def ref_hop_tables():

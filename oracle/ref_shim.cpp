@@ -23,6 +23,7 @@
 //   * the even-odd Schur operator Mhat and the eo CG, built from
 //     apply_dirac (hop = (4+m) psi - D psi) and the reference cg_solve.
 
+#include <latbench/bench.hpp>
 #include <latbench/errors.hpp>
 #include <latbench/fields.hpp>
 #include <latbench/flops.hpp>
@@ -34,12 +35,14 @@
 #include <latbench/solver.hpp>
 #include <latbench/transport.hpp>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace latbench;
@@ -329,51 +332,68 @@ int ref_gauge_unit(const int* global, int n, int rep, double* out) {
 // generator order from RngStream(key_hash{seed,0x47,t,x,y,z,mu})
 // (SURVEY.md §8d pins this normalisation). exp by scaling and squaring with a
 // degree-16 Taylor polynomial on the reference's Mat type.
+Mat near_unit_link(int n, double eps, uint64_t seed, const Coord4& gc, int mu) {
+  const auto& ts = cached_generators(n);
+  RngStream rng(key_hash({seed, 0x47u, static_cast<uint64_t>(gc[0]), static_cast<uint64_t>(gc[1]),
+                          static_cast<uint64_t>(gc[2]), static_cast<uint64_t>(gc[3]),
+                          static_cast<uint64_t>(mu)}));
+  Mat a(n);  // a = i eps H
+  for (size_t k = 0; k < ts.size(); ++k) {
+    const double xi = rng.gauss();
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) a.at(i, j) += Cplx(0.0, eps * xi) * ts[k].at(i, j);
+  }
+  int sq = 0;
+  double nrm = a.max_abs() * n;
+  while (nrm > 0.5) {
+    nrm *= 0.5;
+    ++sq;
+  }
+  a.scale(std::ldexp(1.0, -sq));
+  Mat e = Mat::identity(n), term = Mat::identity(n);
+  for (int k = 1; k <= 16; ++k) {
+    term = term * a;
+    term.scale(1.0 / k);
+    e = e + term;
+  }
+  for (int k = 0; k < sq; ++k) e = e * e;
+  return e;
+}
+
 int ref_gauge_near_unit(const int* global, int n, double eps, uint64_t seed, double* out) {
   SHIM_TRY const Coord4 G = c4(global);
-  const auto& ts = cached_generators(n);
+  (void)cached_generators(n);  // build the cache before the workers read it
   const int64_t V = static_cast<int64_t>(G[0]) * G[1] * G[2] * G[3];
-  for (int64_t s = 0; s < V; ++s) {
-    int64_t r = s;
-    Coord4 gc;
-    gc[3] = r % G[3];
-    r /= G[3];
-    gc[2] = r % G[2];
-    r /= G[2];
-    gc[1] = r % G[1];
-    gc[0] = r / G[1];
-    for (int mu = 0; mu < 4; ++mu) {
-      RngStream rng(key_hash({seed, 0x47u, static_cast<uint64_t>(gc[0]),
-                              static_cast<uint64_t>(gc[1]), static_cast<uint64_t>(gc[2]),
-                              static_cast<uint64_t>(gc[3]), static_cast<uint64_t>(mu)}));
-      Mat a(n);  // a = i eps H
-      for (size_t k = 0; k < ts.size(); ++k) {
-        const double xi = rng.gauss();
-        for (int i = 0; i < n; ++i)
-          for (int j = 0; j < n; ++j) a.at(i, j) += Cplx(0.0, eps * xi) * ts[k].at(i, j);
-      }
-      int sq = 0;
-      double nrm = a.max_abs() * n;
-      while (nrm > 0.5) {
-        nrm *= 0.5;
-        ++sq;
-      }
-      a.scale(std::ldexp(1.0, -sq));
-      Mat e = Mat::identity(n), term = Mat::identity(n);
-      for (int k = 1; k <= 16; ++k) {
-        term = term * a;
-        term.scale(1.0 / k);
-        e = e + term;
-      }
-      for (int k = 0; k < sq; ++k) e = e * e;
-      for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) {
-          const size_t o = ((static_cast<size_t>(s) * 4 + mu) * n * n + i * n + j) * 2;
-          out[o] = e.at(i, j).real();
-          out[o + 1] = e.at(i, j).imag();
-        }
+  // T-split over the host threads (keyed per global site: order-independent)
+  Coord4 grid{1, 1, 1, 1};
+  const int nthreads = static_cast<int>(std::thread::hardware_concurrency());
+  for (int k = nthreads; k > 1; --k)
+    if (G[0] % k == 0) {
+      grid[0] = k;
+      break;
     }
-  }
+  const int64_t per = V / grid[0];
+  run_workers(grid, [&](Worker& w) {
+    for (int64_t s = w.rank() * per; s < (w.rank() + 1) * per; ++s) {
+      int64_t r = s;
+      Coord4 gc;
+      gc[3] = r % G[3];
+      r /= G[3];
+      gc[2] = r % G[2];
+      r /= G[2];
+      gc[1] = r % G[1];
+      gc[0] = r / G[1];
+      for (int mu = 0; mu < 4; ++mu) {
+        const Mat e = near_unit_link(n, eps, seed, gc, mu);
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) {
+            const size_t o = ((static_cast<size_t>(s) * 4 + mu) * n * n + i * n + j) * 2;
+            out[o] = e.at(i, j).real();
+            out[o + 1] = e.at(i, j).imag();
+          }
+      }
+    }
+  });
   SHIM_CATCH
 }
 
@@ -568,30 +588,169 @@ int ref_cg_eo(const int* global, const int* grid, int n, int rep, int bc_time, d
 }
 
 // ---- CPU baseline timing ----------------------------------------------------
+// Per-worker inputs of the BASELINE workloads, generated in parallel on the
+// worker's own interior (keyed per global site, so identical for any worker
+// grid): Haar links via the reference's randomize_gauge_interior, or the
+// near-unit links above (config 3); antiperiodic t as the U_0 sign flip on the
+// last global time slice; then the reference gauge halo exchange
+// (init_gauge_random, proj/src/transport.cpp:223-229, with the flip inserted).
+GaugeField make_links(Worker& w, const ExchangePlan& plan, const Geometry& geo, const Problem& p,
+                      int links, double eps, uint64_t seed, int bc_time) {
+  GaugeField g = make_gauge(geo, p.n, p.rep);
+  if (links == 1) {  // near-unit fundamental links
+    if (p.rep != Representation::Fundamental) throw ConfigError("near-unit links are fundamental only");
+    const size_t nn = static_cast<size_t>(p.n) * p.n;
+    for (int s = 0; s < geo.interior; ++s) {
+      const Coord4 gc = geo.global_coords(s);
+      for (int mu = 0; mu < 4; ++mu) {
+        const Mat e = near_unit_link(p.n, eps, seed, gc, mu);
+        for (int i = 0; i < p.n; ++i)
+          for (int j = 0; j < p.n; ++j) g.cdata[(static_cast<size_t>(s) * 4 + mu) * nn + i * p.n + j] = e.at(i, j);
+      }
+    }
+  } else {
+    randomize_gauge_interior(g, seed);
+  }
+  if (bc_time) {
+    const size_t nn = static_cast<size_t>(g.dr) * g.dr;
+    for (int s = 0; s < geo.interior; ++s) {
+      if (geo.global_coords(s)[0] != geo.global[0] - 1) continue;
+      const size_t base = static_cast<size_t>(s) * 4 * nn;  // mu = 0
+      for (size_t k = 0; k < nn; ++k) {
+        if (g.real_links)
+          g.rdata[base + k] = -g.rdata[base + k];
+        else
+          g.cdata[base + k] = -g.cdata[base + k];
+      }
+    }
+  }
+  halo_exchange(w, plan, g);
+  return g;
+}
+
 // The reference's own Dirac benchmark body (proj/src/bench.cpp:190-248) with a
-// fixed application count: fields generated per worker from the keyed RNG
-// (decomposition invariant), then `napps` apply_dirac calls timed between
-// barriers on the rank-0 steady clock. Input is fixed (no chaining) so norms
-// stay finite for any count; timing is identical to the chained loop.
-int ref_bench_dirac(const int* global, const int* grid, int n, int rep, double mass, uint64_t seed,
-                    int napps, double* seconds) {
+// fixed application count on the BASELINE workload (links kind, antiperiodic
+// t): fields generated per worker, `nwarm` warm-up applications, then
+// `nsamples` samples of `napps` timed applications between barriers, rank-0
+// clock, seconds[k] per sample.
+int ref_bench_dirac(const int* global, const int* grid, int n, int rep, int links, double eps, int bc_time,
+                    double mass, uint64_t seed, int nwarm, int napps, int nsamples, double* seconds) {
   SHIM_TRY const Problem p = make_problem(global, grid, n, rep);
+  if (links == 1) (void)cached_generators(n);
   run_workers(p.grid, [&](Worker& w) {
     const Geometry geo = build_geometry(p.global, p.grid, w.rank(), false);
     const ExchangePlan plan = build_exchange_plan(geo);
-    GaugeField g = init_gauge_random(w, plan, geo, p.n, p.rep, seed);
+    GaugeField g = make_links(w, plan, geo, p, links, eps, seed, bc_time);
     SpinorField a = init_spinor_random(geo, p.dr, seed, 0), b = make_spinor(geo, p.dr);
-    apply_dirac(b, g, a, mass, w, plan);  // warm-up
+    for (int i = 0; i < nwarm; ++i) apply_dirac(b, g, a, mass, w, plan);  // warm-up
     SteadyClock clock;
-    w.barrier();
-    const double t0 = w.rank() == 0 ? clock.seconds() : 0.0;
-    for (int i = 0; i < napps; ++i) apply_dirac(b, g, a, mass, w, plan);
-    w.barrier();
-    const double dt = w.rank() == 0 ? clock.seconds() - t0 : 0.0;
-    const double tot = w.global_sum(dt);
-    if (w.rank() == 0) *seconds = tot;
+    for (int k = 0; k < nsamples; ++k) {
+      w.barrier();
+      const double t0 = w.rank() == 0 ? clock.seconds() : 0.0;
+      for (int i = 0; i < napps; ++i) apply_dirac(b, g, a, mass, w, plan);
+      w.barrier();
+      const double dt = w.rank() == 0 ? clock.seconds() - t0 : 0.0;
+      const double tot = w.global_sum(dt);
+      if (w.rank() == 0) seconds[k] = tot;
+    }
   });
   SHIM_CATCH
 }
+
+// The reference cg_solve (proj/src/solver.cpp:24-82) timed on the BASELINE
+// workload, inputs generated per worker. eo = 0: the reference's own plain CG
+// on H = g5 D g5 D (make_h_operator); eo = 1: the reference cg_solve driven by
+// the composed g5 Mhat g5 Mhat LinearOp (as ref_cg_eo), rhs = even part of
+// spinor field 0. tol > 0: a real solve to tol (at most max_iterations);
+// tol <= 0: a bounded CPU sample of exactly max_iterations iterations with an
+// unreachable tolerance, the NonConvergence at the cap caught. *seconds is
+// the wall time of the whole cg_solve call on the rank-0 clock (setup and,
+// for a solve, the exit true-residual check included), *iterations the
+// iterations run, *true_rel the exit true residual (solve only, else -1),
+// *seconds_per_iteration the solve time / iterations, or for a sample the
+// time difference to a 1-iteration call / (max_iterations - 1), so that the
+// per-solve setup (field allocation, |b|) is not counted per iteration.
+int ref_cg_probe(const int* global, const int* grid, int n, int rep, int links, double eps, int bc_time,
+                 double mass, uint64_t seed, int eo, double tol, int max_iterations, double* seconds,
+                 long* iterations, double* true_rel, double* seconds_per_iteration) {
+  SHIM_TRY const Problem p = make_problem(global, grid, n, rep);
+  if (links == 1) (void)cached_generators(n);
+  run_workers(p.grid, [&](Worker& w) {
+    const Geometry geo = build_geometry(p.global, p.grid, w.rank(), false);
+    const ExchangePlan plan = build_exchange_plan(geo);
+    GaugeField g = make_links(w, plan, geo, p, links, eps, seed, bc_time);
+    SpinorField b = init_spinor_random(geo, p.dr, seed, 0);
+    if (eo) mask_parity(b, 0);
+    SpinorField t1 = make_spinor(geo, p.dr), t2 = make_spinor(geo, p.dr), t3 = make_spinor(geo, p.dr);
+    LinearOp op;
+    if (eo) {
+      op = [&](SpinorField& out, SpinorField& in) {
+        mhat(t3, g, in, mass, w, plan, t1, t2);
+        apply_gamma5(t3);
+        mhat(out, g, t3, mass, w, plan, t1, t2);
+        apply_gamma5(out);
+      };
+    } else {
+      op = make_h_operator(g, mass, w, plan, t1);
+    }
+    SteadyClock clock;
+    CgSettings st;
+    st.tolerance = tol > 0.0 ? tol : 1e-300;
+    st.max_iterations = max_iterations;
+    long its = max_iterations;
+    double trel = -1.0;
+    auto timed = [&](int cap) {  // wall time of one cg_solve call, rank-0 clock
+      st.max_iterations = cap;
+      w.barrier();
+      const double t0 = w.rank() == 0 ? clock.seconds() : 0.0;
+      try {
+        const CgOutcome o = cg_solve(op, b, st, w, clock);
+        its = o.iterations;
+        trel = o.true_rel_residual;
+      } catch (const NonConvergence&) {
+        if (tol > 0.0) throw;
+        its = cap;
+      }
+      w.barrier();
+      const double dt = w.rank() == 0 ? clock.seconds() - t0 : 0.0;
+      return w.global_sum(dt);
+    };
+    double tot = 0.0, per_it = 0.0;
+    if (tol > 0.0 || max_iterations < 2) {
+      tot = timed(max_iterations);
+      per_it = tot / std::max<long>(1, its);
+    } else {  // sample: a 1-iteration call calibrates the setup cost away
+      const double t1 = timed(1);
+      tot = timed(max_iterations);
+      per_it = (tot - t1) / (max_iterations - 1);
+    }
+    if (w.rank() == 0) {
+      *seconds = tot;
+      *iterations = its;
+      *true_rel = trel;
+      *seconds_per_iteration = per_it;
+    }
+  });
+  SHIM_CATCH
+}
+
+#ifdef SHIM_HAVE_REPORT
+// Report interop (proj/src/report.cpp:152-217): parse a format-1 JSON report
+// with the reference's report_from_json and re-emit it with format_report
+// (format 0 text, 1 json, 2 csv). rc 2 (ConfigError) for a report the
+// reference rejects. *len is the full length; out gets at most cap-1 bytes.
+int ref_report_reformat(const char* json_text, int format, char* out, size_t cap, size_t* len) {
+  SHIM_TRY const BenchReport r = report_from_json(json_text);
+  const ReportFormat f = format == 0 ? ReportFormat::Text : format == 1 ? ReportFormat::Json : ReportFormat::Csv;
+  const std::string txt = format_report(r, f);
+  *len = txt.size();
+  if (cap > 0) {
+    const size_t n = std::min(cap - 1, txt.size());
+    std::memcpy(out, txt.data(), n);
+    out[n] = 0;
+  }
+  SHIM_CATCH
+}
+#endif
 
 }  // extern "C"

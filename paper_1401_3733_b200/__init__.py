@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -140,6 +141,7 @@ def lib():
             "lbcu_ctx_local": (C.c_int, [_vp, _ip]),
             "lbcu_barrier": (C.c_int, [_vp]),
             "lbcu_ctx_kernel_launches": (C.c_longlong, [_vp]),
+            "lbcu_ctx_cached_solves": (C.c_longlong, [_vp]),
             "lbcu_event_record": (C.c_int, [_vp, C.c_int]),
             "lbcu_event_elapsed_ms": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
             "lbcu_gauge_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
@@ -271,12 +273,49 @@ def plan_faces(global_, grid, rank, input_parity):
     return list(partner), list(count), sites
 
 
+# ---------------------------------------------------------------- ownership
+def _release(destroy: str, handle):
+    """Finalizer body: free one library handle (never raises)."""
+    try:
+        if _lib is not None and handle:
+            getattr(_lib, destroy)(handle)
+    except Exception:  # pragma: no cover - interpreter shutdown
+        pass
+
+
+class _Owned:
+    """A library handle freed exactly once: by close(), or by a finalizer when
+    the Python object is collected (weakref.finalize also runs at exit, in
+    reverse creation order, so fields go before their context and contexts
+    before their world). A context closes its live fields first, so nothing
+    is ever freed through a dangling context."""
+
+    _destroy = ""
+
+    def _own(self, handle, parent=None):
+        self._h = handle
+        self._fin = weakref.finalize(self, _release, self._destroy, handle)
+        self._children = weakref.WeakSet()
+        if parent is not None:
+            parent._children.add(self)
+
+    def close(self):
+        for ch in list(getattr(self, "_children", ())):
+            ch.close()
+        fin = getattr(self, "_fin", None)
+        if fin is not None:
+            fin()
+        self._h = None
+
+
 # ---------------------------------------------------------------- worlds
-class World:
+class World(_Owned):
     """Transport shared by the ranks of one decomposition (WorkerGroup)."""
 
+    _destroy = "lbcu_world_destroy"
+
     def __init__(self, handle):
-        self._h = handle
+        self._own(handle)
 
     @classmethod
     def single(cls):
@@ -320,14 +359,11 @@ class World:
         """Collective: direct peer-memory halos (True) or message exchange."""
         _check(lib().lbcu_world_set_direct(self._h, 1 if on else 0))
 
-    def close(self):
-        if self._h:
-            lib().lbcu_world_destroy(self._h)
-            self._h = None
 
-
-class Context:
+class Context(_Owned):
     """One rank: Geometry + ExchangePlan + Worker + a CUDA stream."""
+
+    _destroy = "lbcu_ctx_destroy"
 
     def __init__(self, global_, grid=(1, 1, 1, 1), rank=0, device=0, world: Optional[World] = None,
                  enforce_floor=False):
@@ -338,7 +374,7 @@ class Context:
         h = _vp()
         _check(lib().lbcu_ctx_create(world._h if world else None, self.rank, int(device),
                                      _i4(self.global_), _i4(self.grid), int(enforce_floor), C.byref(h)))
-        self._h = h
+        self._own(h)
         loc = (C.c_int * 4)()
         _check(lib().lbcu_ctx_local(h, loc))
         self.local = tuple(loc)
@@ -357,6 +393,10 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib().lbcu_ctx_kernel_launches(self._h))
 
+    def cached_solves(self) -> int:
+        """Instantiated CG solve graphs held by the context."""
+        return int(lib().lbcu_ctx_cached_solves(self._h))
+
     def event_record(self, slot: int):
         _check(lib().lbcu_event_record(self._h, int(slot)))
 
@@ -365,20 +405,12 @@ class Context:
         _check(lib().lbcu_event_elapsed_ms(self._h, int(a), int(b), C.byref(ms)))
         return float(ms.value)
 
-    def close(self):
-        if getattr(self, "_h", None):
-            lib().lbcu_ctx_destroy(self._h)
-            self._h = None
-
-    def __del__(self):  # pragma: no cover - interpreter shutdown order
-        try:
-            self.close()
-        except Exception:
-            pass
 
 
-class GaugeField:
+class GaugeField(_Owned):
     """latbench::GaugeField on the device (fields.hpp:37-57)."""
+
+    _destroy = "lbcu_gauge_destroy"
 
     def __init__(self, ctx: Context, group_rank: int, rep=FUNDAMENTAL, bc_time=ANTIPERIODIC_T):
         rep = _REP_NAMES.get(rep, rep) if isinstance(rep, str) else rep
@@ -387,7 +419,7 @@ class GaugeField:
         self.real_links = rep_is_real(rep)
         h = _vp()
         _check(lib().lbcu_gauge_create(ctx._h, self.group_rank, self.rep, self.bc_time, C.byref(h)))
-        self._h = h
+        self._own(h, ctx)
 
     @property
     def host_shape(self):
@@ -432,20 +464,17 @@ class GaugeField:
         _check(lib().lbcu_gauge_download(self._h, out.ctypes.data_as(_dp)))
         return out
 
-    def close(self):
-        if getattr(self, "_h", None):
-            lib().lbcu_gauge_destroy(self._h)
-            self._h = None
 
-
-class SpinorField:
+class SpinorField(_Owned):
     """latbench::SpinorField on the device (fields.hpp:15-24); subset FULL/EVEN/ODD."""
+
+    _destroy = "lbcu_spinor_destroy"
 
     def __init__(self, ctx: Context, dr: int, subset=FULL):
         self.ctx, self.dr, self.subset = ctx, int(dr), int(subset)
         h = _vp()
         _check(lib().lbcu_spinor_create(ctx._h, self.dr, self.subset, C.byref(h)))
-        self._h = h
+        self._own(h, ctx)
 
     @property
     def host_shape(self):
@@ -475,11 +504,6 @@ class SpinorField:
 
     def download_ptr(self, ptr: int):
         _check(lib().lbcu_spinor_download(self._h, C.cast(C.c_void_p(ptr), _dp)))
-
-    def close(self):
-        if getattr(self, "_h", None):
-            lib().lbcu_spinor_destroy(self._h)
-            self._h = None
 
 
 # ---------------------------------------------------------------- operators

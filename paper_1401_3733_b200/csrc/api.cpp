@@ -289,7 +289,10 @@ int lbcu_ctx_create(lbcu_world w, int rank, int device, const int global[4], con
   LBCU_CUDA(cudaSetDevice(device));
   w->t->bind_device(device);
   LBCU_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-  LBCU_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;  // the halo pack runs ahead of the interior stencil
+  LBCU_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  LBCU_CUDA(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, prio_hi));
+  LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
   LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_comm, cudaEventDisableTiming));
   for (auto& e : ctx->ev) LBCU_CUDA(cudaEventCreate(&e));
@@ -341,6 +344,8 @@ int lbcu_ctx_destroy(lbcu_ctx c) {
   if (!c) return LBCU_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  cudaStreamSynchronize(c->comm_stream);
+  graph_cache_clear(c);
   host_pipe_release(c);
   for (auto& kv : c->scratch) free_spinor(kv.second);
   for (auto& kv : c->halo)
@@ -361,6 +366,7 @@ int lbcu_ctx_destroy(lbcu_ctx c) {
   if (c->dhist) cudaFree(c->dhist);
   if (c->staging) cudaFree(c->staging);
   for (auto& e : c->ev) cudaEventDestroy(e);
+  cudaEventDestroy(c->ev_fork);
   cudaEventDestroy(c->ev_pack);
   for (int e = 0; e < 2; ++e)
     if (c->ev_cg[e]) cudaEventDestroy(c->ev_cg[e]);
@@ -408,6 +414,9 @@ int lbcu_allreduce_sum(lbcu_ctx c, double* values, int n) {
 }
 
 long long lbcu_ctx_kernel_launches(lbcu_ctx c) { return c ? c->launches : -1; }
+long long lbcu_ctx_cached_solves(lbcu_ctx c) {
+  return c ? static_cast<long long>(graph_cache_size(c)) : -1;
+}
 
 int lbcu_event_record(lbcu_ctx c, int slot) {
   API_BEGIN
@@ -453,6 +462,7 @@ int lbcu_gauge_upload(lbcu_gauge g, const double* host) {
   API_BEGIN
   need(g && host, "lbcu_gauge_upload: null argument");
   bind(g->ctx);
+  graph_cache_forget(g->ctx, g);  // the link buffer and its storage format may change
   gauge_upload(g->ctx, g, host);
   API_END
 }
@@ -472,6 +482,7 @@ int lbcu_gauge_generate(lbcu_gauge g, int links, uint64_t seed, double eps) {
     throw Error(LBCU_CONFIG_ERROR, "unknown link generator");
   lbcu_ctx_s* c = g->ctx;
   bind(c);
+  graph_cache_forget(c, g);
   if (g->rep == LBCU_REP_ANTISYMMETRIC && g->n == 4 && g->compact_ok) {
     // SU(4) fundamental elements -> real SO(6) storage (or kept as AS4)
     gauge_adopt_fundamental(c, g, gauge_generate_dense(c, g, links, seed, eps, true));
@@ -493,6 +504,7 @@ int lbcu_gauge_upload_fundamental(lbcu_gauge g, const double* host) {
   API_BEGIN
   need(g && host, "lbcu_gauge_upload_fundamental: null argument");
   bind(g->ctx);
+  graph_cache_forget(g->ctx, g);
   gauge_upload_fundamental(g->ctx, g, host);
   API_END
 }
@@ -517,6 +529,7 @@ int lbcu_gauge_destroy(lbcu_gauge g) {
   if (!g) return LBCU_OK;
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
+  graph_cache_forget(g->ctx, g);
   cudaFree(g->base);
   delete g;
   API_END
@@ -554,6 +567,7 @@ int lbcu_spinor_destroy(lbcu_spinor s) {
   if (!s) return LBCU_OK;
   cudaSetDevice(s->ctx->device);
   cudaStreamSynchronize(s->ctx->stream);
+  graph_cache_forget(s->ctx, s);
   free_spinor(s);
   API_END
 }

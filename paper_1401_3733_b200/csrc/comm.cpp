@@ -60,26 +60,36 @@ struct ThreadTransport final : Transport {
     for (auto& ev : events_)
       for (auto e : ev)
         if (e) cudaEventDestroy(e);
+    for (auto& kv : arenas_)  // the world owns the receive arenas (map_arena)
+      for (void* a : kv.second)
+        if (a) cudaFree(a);
   }
   int nranks() const override { return n_; }
   bool capturable() const override { return false; }
 
   // ---- direct mode (peer arenas are plain device pointers in one process)
-  bool direct() const override { return direct_; }
-  void set_direct(bool on) override { direct_ = on; }
-  void attach(int rank, int) override {
-    if (!direct_) return;
+  bool direct() const override { return direct_.load(std::memory_order_acquire); }
+  // one thread flips the shared mode; callers bracket it with barriers so no
+  // rank is inside an exchange (test_direct_halo_toggle_matches)
+  void set_direct(bool on) override { direct_.store(on, std::memory_order_release); }
+  void attach(int rank, int) override {  // events exist even if direct mode is switched on later
     for (auto& e : events_[rank])
       if (!e) LBCU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  // Collective. The world takes ownership of `local` (freed at teardown);
+  // re-mapping a key (a new context on the same world) frees the rank's old
+  // arena once every rank has switched to the new ones.
   void map_arena(int rank, int key, void* local, size_t) override {
+    void* old = nullptr;
     {
       std::lock_guard<std::mutex> lk(m_);
       auto& v = arenas_[key];
       if (v.empty()) v.assign(n_, nullptr);
+      old = v[rank];
       v[rank] = local;
     }
     sync();
+    if (old && old != local) cudaFree(old);
   }
   void* peer_arena(int, int key, int peer) const override {
     std::lock_guard<std::mutex> lk(m_);
@@ -153,7 +163,7 @@ struct ThreadTransport final : Transport {
     return tree(k, lo, mid) + tree(k, mid, hi);
   }
   int n_;
-  bool direct_;
+  std::atomic<bool> direct_;
   mutable std::mutex m_;
   std::condition_variable cv_;
   int arrived_ = 0;
@@ -318,24 +328,16 @@ struct IpcTransport final : Transport {
   ~IpcTransport() override {
     // collective teardown: nobody closes its mappings while a peer may still
     // be inside a collective call (bounded wait, never throws)
-    if (sh_) {
-      const uint32_t g = sh_->gen.load(std::memory_order_acquire);
-      if (sh_->arrive.fetch_add(1, std::memory_order_acq_rel) + 1 == static_cast<uint32_t>(n_)) {
-        sh_->arrive.store(0, std::memory_order_relaxed);
-        sh_->gen.fetch_add(1, std::memory_order_release);
-      } else {
-        const auto t0 = std::chrono::steady_clock::now();
-        while (sh_->gen.load(std::memory_order_acquire) == g &&
-               std::chrono::steady_clock::now() - t0 < std::chrono::seconds(30))
-          sched_yield();
-      }
-    }
+    if (sh_) bounded_barrier();
     for (auto& kv : peer_mem_)
-      for (void* q : kv.second)
-        if (q) cudaIpcCloseMemHandle(q);
+      for (int q = 0; q < static_cast<int>(kv.second.size()); ++q)
+        if (q != rank_ && kv.second[q]) cudaIpcCloseMemHandle(kv.second[q]);
     for (int q = 0; q < n_; ++q)
       for (int e = 0; e < 2; ++e)
         if (ev_[q][e]) cudaEventDestroy(ev_[q][e]);
+    // an exported arena is freed only after every importer closed it
+    if (sh_ && !own_arenas_.empty()) bounded_barrier();
+    for (auto& kv : own_arenas_) cudaFree(kv.second);
     if (sh_) munmap(sh_, sizeof(IpcShared));
   }
   int nranks() const override { return n_; }
@@ -361,17 +363,25 @@ struct IpcTransport final : Transport {
     host_barrier();
     attached_ = true;
   }
+  // Collective. The world owns `local` from here on: it is freed at world
+  // teardown, or when the key is re-mapped (a new context on the same world)
+  // after every peer has closed its mapping of the old arena.
   void map_arena(int rank, int key, void* local, size_t) override {
     if (key < 0 || key >= kIpcMaxKeys) throw Error(LBCU_TRANSPORT_ERROR, "ipc world: arena key out of range");
     LBCU_CUDA(cudaIpcGetMemHandle(&sh_->mem[key][rank], local));
     host_barrier();
     auto& v = peer_mem_[key];
+    for (int q = 0; q < static_cast<int>(v.size()); ++q)  // a previous context's arenas
+      if (q != rank && v[q]) cudaIpcCloseMemHandle(v[q]);
     v.assign(n_, nullptr);
     for (int q = 0; q < n_; ++q)
       if (q != rank)
         LBCU_CUDA(cudaIpcOpenMemHandle(&v[q], sh_->mem[key][q], cudaIpcMemLazyEnablePeerAccess));
     v[rank] = local;
     host_barrier();
+    void*& mine = own_arenas_[key];
+    if (mine && mine != local) cudaFree(mine);  // every peer closed it before the barrier
+    mine = local;
   }
   void* peer_arena(int, int key, int peer) const override {
     auto it = peer_mem_.find(key);
@@ -417,6 +427,19 @@ struct IpcTransport final : Transport {
       }
     }
   }
+  // teardown barrier: bounded wait, never throws
+  void bounded_barrier() {
+    const uint32_t g = sh_->gen.load(std::memory_order_acquire);
+    if (sh_->arrive.fetch_add(1, std::memory_order_acq_rel) + 1 == static_cast<uint32_t>(n_)) {
+      sh_->arrive.store(0, std::memory_order_relaxed);
+      sh_->gen.fetch_add(1, std::memory_order_release);
+      return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    while (sh_->gen.load(std::memory_order_acquire) == g &&
+           std::chrono::steady_clock::now() - t0 < std::chrono::seconds(30))
+      sched_yield();
+  }
   // generation barrier over the shared segment
   void host_barrier() {
     const uint32_t g = sh_->gen.load(std::memory_order_acquire);
@@ -440,6 +463,7 @@ struct IpcTransport final : Transport {
   bool attached_ = false;
   bool direct_ = true;
   std::map<int, std::vector<void*>> peer_mem_;
+  std::map<int, void*> own_arenas_;  // this rank's receive arenas, by key
 };
 
 }  // namespace

@@ -951,9 +951,17 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     }
   }
   PA.first[PA.njobs] = pack_blocks;
+  // The pack (and, for message transports, the exchange) runs on the
+  // high-priority comm stream, forked from the compute stream, so the
+  // interior launch below runs concurrently with it: with a direct transport
+  // the pack's NVLink stores into the peers' arenas overlap the interior
+  // stencil; with NCCL the pack + send/recv do.
+  const cudaStream_t cs = ctx->comm_stream;
+  LBCU_CUDA(cudaEventRecord(ctx->ev_fork, s));
+  LBCU_CUDA(cudaStreamWaitEvent(cs, ctx->ev_fork, 0));
   if (pack_blocks > 0) {
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-      pack_kernel<LBCU_TPARAMS(Dc, Rc, Fc)><<<pack_blocks, kBlock, 0, s>>>(PA);
+      pack_kernel<LBCU_TPARAMS(Dc, Rc, Fc)><<<pack_blocks, kBlock, 0, cs>>>(PA);
     });
     ctx->launches += 1;
     LBCU_CUDA(cudaGetLastError());
@@ -988,10 +996,10 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   };
   // interior sites (no halo dependency) run on the compute stream while the
   // halos travel; boundary sites wait for them. Direct transports: the pack
-  // kernel already stored into the peers, its completion is posted as an
-  // event that the peers' streams wait on before their boundary launch.
-  if (direct) T->post(ctx->rank, epoch, s);
-  else LBCU_CUDA(cudaEventRecord(ctx->ev_pack, s));
+  // kernel stores into the peers, its completion is posted as an event that
+  // the peers' compute streams wait on before their boundary launch.
+  if (direct) T->post(ctx->rank, epoch, cs);
+  LBCU_CUDA(cudaEventRecord(ctx->ev_pack, cs));
   // warp-shared z hops for a contiguous interior whose warps cover whole z-rows
   const int hz = geo.local[3] / 2;
   for (int gi = 0; gi < ngroups; ++gi) {
@@ -1005,15 +1013,18 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     ctx->launches += 1;
   }
   if (direct) {
+    // join the own pack (it reads `in`, which later work on s may overwrite;
+    // the chain pack(k+2) after boundary(k+1) keeps the arena slots safe),
+    // then every peer's pack of this exchange
+    LBCU_CUDA(cudaStreamWaitEvent(s, ctx->ev_pack, 0));
     std::vector<int> peers;
     for (int f = 0; f < 8; ++f)
       if (ctx->plan.count[f] && std::find(peers.begin(), peers.end(), ctx->plan.partner[f]) == peers.end())
         peers.push_back(ctx->plan.partner[f]);
     T->await(ctx->rank, epoch, peers, s);
   } else {
-    LBCU_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_pack, 0));
-    T->exchange(ctx->rank, msgs, ctx->comm_stream);
-    LBCU_CUDA(cudaEventRecord(ctx->ev_comm, ctx->comm_stream));
+    T->exchange(ctx->rank, msgs, cs);  // after the interior launch: may block the host
+    LBCU_CUDA(cudaEventRecord(ctx->ev_comm, cs));
     LBCU_CUDA(cudaStreamWaitEvent(s, ctx->ev_comm, 0));
   }
   for (int gi = 0; gi < ngroups; ++gi) {

@@ -99,8 +99,10 @@ struct Transport {
   virtual void set_direct(bool on) {
     if (on) throw Error(LBCU_TRANSPORT_ERROR, "transport has no direct halo mode");
   }
-  // collective, once per key: register this rank's receive arena and map
-  // every peer's (same size and layout on every rank)
+  // collective, once per key and context: register this rank's receive arena
+  // and map every peer's (same size and layout on every rank). The transport
+  // takes ownership of `local` and frees it at teardown or when the key is
+  // mapped again, once no peer can still store into it.
   virtual void map_arena(int /*rank*/, int /*key*/, void* /*local*/, size_t /*bytes*/) {
     throw Error(LBCU_TRANSPORT_ERROR, "transport has no peer-memory arenas");
   }

@@ -42,7 +42,8 @@ struct HaloBufs {
   double2* send[2][8] = {};  // by output parity, face
   double2* recv[2][8] = {};
   // direct transports: one receive arena [parity][face][epoch & 1] of `slot`
-  // double2 each, mapped by every peer (Transport::map_arena)
+  // double2 each, mapped by every peer and owned by the world's transport
+  // (Transport::map_arena frees it; lbcu_ctx_destroy does not)
   double2* arena = nullptr;
   size_t slot = 0;
   size_t cap = 0;  // double2 per buffer
@@ -58,8 +59,8 @@ struct lbcu_ctx_s {
   lbcu::FacePlan plan;
   lbcu::DevGeo dgeo{};
   cudaStream_t stream = nullptr;
-  cudaStream_t comm_stream = nullptr;  // halo exchange (decomposed runs)
-  cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
+  cudaStream_t comm_stream = nullptr;  // halo pack + exchange (decomposed runs), high priority
+  cudaEvent_t ev_fork = nullptr, ev_pack = nullptr, ev_comm = nullptr;
   cudaEvent_t ev[16] = {};
   // reduction workspace
   double* partials = nullptr;
@@ -147,6 +148,13 @@ void* gauge_generate_dense(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, int links, ui
 void dphi_host_batch(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, double mass, int n,
                      const double* const* in, double* const* out);
 void host_pipe_release(lbcu_ctx_s* ctx);
+
+// CG graph cache (solver.cpp): drop every instantiated solve that names a
+// handle (spinor or gauge) before it is freed or its links are replaced, and
+// all of a context's solves when it is destroyed
+void graph_cache_forget(const lbcu_ctx_s* ctx, const void* handle);
+void graph_cache_clear(const lbcu_ctx_s* ctx);
+size_t graph_cache_size(const lbcu_ctx_s* ctx);
 
 // helpers in api.cpp
 lbcu_spinor_s* scratch_spinor(lbcu_ctx_s* ctx, int dr, int subset, int slot);

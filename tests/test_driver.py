@@ -80,3 +80,38 @@ def test_run_suite_on_device(tmp_path, grid, eo):
 def test_check_subcommand(tmp_path):
     r = run(["check"], tmp_path, SMALL.format(grid="1x1x1x1", eo="true"))
     assert r.returncode == 0 and "consistency passed" in r.stdout, r.stdout + r.stderr
+
+
+def _ref_report_available():
+    try:
+        import oracle as O
+        return hasattr(O.ref_lib(), "ref_report_reformat")
+    except Exception:  # noqa: BLE001
+        return False
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not _ref_report_available(), reason="reference built without report.cpp")
+def test_run_report_round_trips_through_reference_reader(tmp_path):
+    """Format-1 interop (proj/src/report.cpp:152-217): the driver's JSON report
+    parses with the reference's report_from_json, which re-emits the same
+    fields, and the reference's CSV writer reproduces the driver's CSV of the
+    same report byte for byte."""
+    import oracle as O
+    prefix = tmp_path / "rep"
+    r = run(["run", "--format", "json", "--emit-all", str(prefix)], tmp_path, SMALL.format(grid="1x1x1x1", eo="true"))
+    assert r.returncode == 0, r.stderr
+    ours = (tmp_path / "rep.json").read_text()
+    theirs = json.loads(O.ref_report_reformat(ours, "json"))
+    mine = json.loads(ours)
+    for k in ("format_version", "regime", "timestamp", "geometry", "group_rank", "representation", "mass", "seed",
+              "model"):
+        assert theirs[k] == mine[k], k
+    assert [k["kernel"] for k in theirs["kernels"]] == ["sqnorm", "muladd", "dirac"]
+    for a, b in zip(theirs["kernels"], mine["kernels"]):
+        assert a == b
+    c = dict(mine["consistency"])
+    c.pop("solver")
+    assert theirs["consistency"] == c
+    assert O.ref_report_reformat(ours, "csv") == (tmp_path / "rep.csv").read_text()
+    assert "dirac" in O.ref_report_reformat(ours, "text")

@@ -5,7 +5,8 @@
 * size-independent properties on the device: gamma5-hermiticity
   <phi, g5 D g5 psi> = conj <psi, D phi>, linearity, and the Schur relation
   D (x_e - D_oe x_e / A) = (Mhat x_e, 0);
-* the eo CG converges with the true residual below 2 tol.
+* eo and plain CG iteration counts within +-1 of the unmodified reference's
+  at full size (tests/golden/cg_cfg*.npz), the true residual below 2 tol.
 """
 import os
 
@@ -92,14 +93,39 @@ def test_full_size_identities(c):
     assert np.abs(full[~even]).max() < 1e-12 * np.abs(full[even]).max()
 
 
-@pytest.mark.parametrize("c", [2, 3, 4, 5])
+def golden_cg(c):
+    """The unmodified reference's CG at this config's full size
+    (tests/golden/make_fullsize_cg.py): plain cg_solve(make_h_operator) and
+    the cg_solve driven by the composed eo operator."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"cg_cfg{c}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    return np.load(path)
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
 def test_full_size_eo_cg(c):
+    """eo CG iterations within +-1 of the reference-composed eo CG at full size."""
     cfg, ctx, gauge, dr = setup_cfg(c)
     rhs = lb.SpinorField(ctx, dr, lb.EVEN).randomize(1, 0)
     o = lb.cg_solve_eo(gauge, cfg["mass"], rhs, lb.CgSettings(cfg["tol"], 5000))
+    z = golden_cg(c)
     assert o.true_rel_residual < 2 * cfg["tol"]
-    # survey: 23 eo iterations for the Haar configs, ~110-130 for config 3
-    if c != 3:
-        assert abs(o.iterations - 23) <= 1
-    else:
-        assert 100 <= o.iterations <= 140
+    assert abs(o.iterations - int(z["eo_iterations"])) <= 1, (o.iterations, int(z["eo_iterations"]))
+    # the residual history follows the reference's until rounding separates them
+    k = min(10, o.iterations, len(z["eo_history"]))
+    assert np.allclose(o.residual_history[:k], z["eo_history"][:k], rtol=1e-6)
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_full_size_plain_cg(c):
+    """Plain CG on D^dag D (the reference's own consistency solve, solver.cpp:24-82)
+    within +-1 of the reference's iteration count at full size."""
+    cfg, ctx, gauge, dr = setup_cfg(c)
+    rhs = lb.SpinorField(ctx, dr).randomize(1, 0)
+    o = lb.cg_solve_h(gauge, cfg["mass"], rhs, lb.CgSettings(cfg["tol"], 5000))
+    z = golden_cg(c)
+    assert o.true_rel_residual < 2 * cfg["tol"]
+    assert abs(o.iterations - int(z["h_iterations"])) <= 1, (o.iterations, int(z["h_iterations"]))
+    k = min(10, o.iterations, len(z["h_history"]))
+    assert np.allclose(o.residual_history[:k], z["h_history"][:k], rtol=1e-6)

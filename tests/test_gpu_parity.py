@@ -120,6 +120,82 @@ def test_blas_matches_reference(n, rep):
     assert np.array_equal(b.download(), w)
 
 
+@pytest.mark.parametrize("n,rep", REPS[:2], ids=REP_IDS[:2])
+def test_xpay_axpy_copy_zero_match_reference(n, rep):
+    """kernels.cpp:45-49,75-104: xpay y = x + a y, axpy y += a x, copy, zero —
+    against the reference's formulas on the same fields (bit-exact: one
+    complex multiply-add per component, no reduction)."""
+    L = [4, 4, 6, 4]
+    dr = lb.rep_dim(rep, n)
+    ctx = lb.Context(L)
+    s0 = lb.init_spinor_random(L, dr, 1, 0)
+    s1 = lb.init_spinor_random(L, dr, 1, 1)
+    a = 0.3 - 1.7j
+    x, y = lb.SpinorField(ctx, dr).upload(s0), lb.SpinorField(ctx, dr).upload(s1)
+    lb.xpay(y, a, x)
+    assert rel_l2(y.download(), s0 + a * s1) < 1e-15
+    y.upload(s1)
+    lb.axpy(y, a, x)
+    assert rel_l2(y.download(), s1 + a * s0) < 1e-15
+    lb.copy_interior(y, x)
+    assert np.array_equal(y.download(), s0)
+    lb.zero_interior(y)
+    assert not y.download().any()
+    # parity subsets: xpay on EVEN fields touches even sites only
+    even = O.parity_mask(L)
+    xe, ye = lb.SpinorField(ctx, dr, lb.EVEN).upload(s0), lb.SpinorField(ctx, dr, lb.EVEN).upload(s1)
+    lb.xpay(ye, a, xe)
+    got = ye.download()
+    assert rel_l2(got[even], (s0 + a * s1)[even]) < 1e-15 and not got[~even].any()
+
+
+def test_cg_graph_cache_follows_field_lifetimes():
+    """The cached CG graph (one per context + field set) is dropped when a
+    field it names is destroyed or the links are re-uploaded: a re-upload
+    that changes the link storage format, and fields re-created at a recycled
+    address, still solve correctly."""
+    L = [8, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, 3, lb.FUNDAMENTAL)
+    rhs = lb.SpinorField(ctx, dr, lb.EVEN).upload(s)
+    x = lb.SpinorField(ctx, dr, lb.EVEN)
+    st = lb.CgSettings(1e-10, 500)
+    ref = O.port_cg(L, 1, 1, 0.1, g, s, 1e-10)
+    o1 = lb.cg_solve_eo(gauge, 0.1, rhs, st, x)
+    assert ctx.cached_solves() == 1
+    lb.cg_solve_eo(gauge, 0.1, rhs, st, x)
+    assert ctx.cached_solves() == 1  # replayed, not re-captured
+    assert gauge.storage()[0] == "r12"
+    gauge.set_compact(False).upload(g)  # new link buffer, dense format
+    assert ctx.cached_solves() == 0 and gauge.storage()[0] == "full"
+    o2 = lb.cg_solve_eo(gauge, 0.1, rhs, st, x)
+    assert abs(o2.iterations - ref["iterations"]) <= 1 and o2.true_rel_residual < 2e-10
+    assert rel_l2(o2.solution.download(), o1.solution.download()) < 1e-9
+    x.close()
+    assert ctx.cached_solves() == 0
+    for _ in range(3):  # handles recycled at the same addresses
+        x = lb.SpinorField(ctx, dr, lb.EVEN)
+        o3 = lb.cg_solve_eo(gauge, 0.1, rhs, st, x)
+        assert o3.iterations == o2.iterations and rel_l2(x.download(), o2.solution.download()) < 1e-12
+        x.close()
+    gauge.close()
+    assert ctx.cached_solves() == 0
+
+
+def test_fields_are_freed_with_their_context():
+    """Python fields free their device memory when collected, and a context
+    closes its live fields before itself (no use of a dangling context)."""
+    import gc
+    L = [8, 8, 8, 8]
+    ctx = lb.Context(L)
+    fs = [lb.SpinorField(ctx, 3) for _ in range(4)]
+    g = lb.GaugeField(ctx, 3)
+    del fs
+    gc.collect()
+    assert len(ctx._children) == 1
+    ctx.close()
+    assert g._h is None
+
+
 @pytest.mark.parametrize("n,rep", REPS, ids=REP_IDS)
 def test_cg_h_matches_reference(n, rep):
     L = [8, 4, 4, 4]

@@ -200,3 +200,102 @@ def test_port_cg_matches_reference_iterations():
         pe = O.port_cg(L, 1, 1, 0.05, g, s, 1e-10)
         assert abs(pe["iterations"] - refe["iterations"]) <= 1
         assert rel_l2(pe["x"], refe["x"]) < 1e-8
+
+
+@needs_ref
+def test_cpu_baseline_entry_points_run_the_baseline_workload():
+    """bench.py's CPU legs: ref_cg_probe solves to the same iteration counts as
+    the global-array reference CG on the same inputs (keyed per worker:
+    decomposition-invariant), and its bounded-sample mode runs exactly the
+    requested iterations; ref_bench_dirac returns one time per sample."""
+    L, n, rep, m = [8, 8, 8, 8], 3, O.FUNDAMENTAL, 0.1
+    z = np.load(os.path.join(GOLD, "cfg1.npz"))
+    for grid in ([1, 1, 1, 1], [2, 1, 1, 2]):
+        h = O.ref_cg_probe(L, grid, n, rep, m, 1, False, 1000, tol=1e-10)
+        e = O.ref_cg_probe(L, grid, n, rep, m, 1, True, 1000, tol=1e-10)
+        assert h["iterations"] == int(z["cg_h_iterations"]) and h["true_rel_residual"] < 2e-10
+        assert e["iterations"] == int(z["cg_eo_iterations"]) and e["true_rel_residual"] < 2e-10
+    p = O.ref_cg_probe(L, [2, 1, 1, 1], n, rep, m, 1, True, 4, tol=0.0)
+    assert p["iterations"] == 4 and p["true_rel_residual"] == -1.0 and p["seconds"] > 0
+    t = O.ref_bench_dirac(L, [2, 1, 1, 1], n, rep, m, 1, 3, nsamples=3)
+    assert len(t) == 3 and min(t) > 0
+    # near-unit links (config 3's generator) through the same entry points
+    nu = O.ref_cg_probe([4, 4, 4, 4], [1, 1, 1, 1], 3, rep, 0.1, 1, True, 500, tol=1e-10, links=O.LINKS_NEAR_UNIT)
+    assert nu["true_rel_residual"] < 2e-10 and nu["iterations"] > 0
+
+
+@needs_ref
+def test_near_unit_generator_parallel_matches_golden():
+    """The threaded near-unit generator reproduces the committed fixture."""
+    z = golden("near_unit")
+    with O.exact_reference():  # the fixture came from the FMA-free build
+        assert np.array_equal(O.ref_gauge_near_unit([2, 2, 2, 2], 3, 0.3, 1), z["links"])
+
+
+REPORT = {
+    "format_version": 1, "regime": "balance", "timestamp": "2026-10-20T00:00:00Z",
+    "geometry": {"lattice": [16, 8, 8, 8], "grid": [1, 1, 1, 1], "local": [16, 8, 8, 8], "workers": 1},
+    "group_rank": 3, "representation": "fundamental", "mass": 0.1, "seed": 1,
+    "kernels": [{"kernel": k, "iterations": 7, "seconds": 0.25, "flops": f * 7 * 8192, "flops_per_sec": 1.5e9,
+                 "flops_per_sec_per_worker": 1.5e9, "short_run": False, "reference_ratio": None}
+                for k, f in (("sqnorm", 48), ("muladd", 96), ("dirac", 1512))],
+    "consistency": {"status": "passed", "iterations": 23, "residual": 4.2e-11, "seconds": 0.001, "solver": "eo"},
+    "model": {"sqnorm_flops_per_site": 48, "muladd_flops_per_site": 96, "dirac_flops_per_site": 1512,
+              "halo_bytes_per_exchange": 0, "dirac_intensity": 0.0},
+    "device": "B200 (sm_100a), latbench-b200",
+}
+
+
+@needs_ref
+def test_report_reader_interop():
+    """report.cpp:182-217: the reference's report_from_json accepts the
+    driver's format-1 JSON (extra keys ignored) and round-trips every field;
+    a format_version it does not know is a ConfigError (rc 2)."""
+    import json
+    if not hasattr(O.ref_lib(), "ref_report_reformat"):
+        pytest.skip("reference built without report.cpp")
+    back = json.loads(O.ref_report_reformat(json.dumps(REPORT), "json"))
+    for k in ("format_version", "regime", "timestamp", "geometry", "group_rank", "representation", "mass", "seed",
+              "kernels", "model"):
+        assert back[k] == REPORT[k], k
+    assert back["consistency"] == {k: v for k, v in REPORT["consistency"].items() if k != "solver"}
+    csv = O.ref_report_reformat(json.dumps(REPORT), "csv").splitlines()
+    assert csv[0] == "kernel,iterations,seconds,flops,flops_per_sec,flops_per_sec_per_worker"
+    assert csv[3].startswith("dirac,7,2.500000000e-01,")
+    bad = dict(REPORT, format_version=2)
+    with pytest.raises(O.OracleError) as e:
+        O.ref_report_reformat(json.dumps(bad), "json")
+    assert e.value.code == 2
+
+
+@needs_ref
+def test_b200_driver_report_reads_back_in_the_reference():
+    """A report written by the B200 driver (tools/latbench_b200 run --emit-all
+    on the GPU box, committed as tests/golden/report_b200.*) parses with the
+    reference's report_from_json, and the reference's own writers reproduce
+    the driver's CSV byte for byte and its JSON field for field."""
+    import json
+    if not hasattr(O.ref_lib(), "ref_report_reformat"):
+        pytest.skip("reference built without report.cpp")
+    ours = open(os.path.join(GOLD, "report_b200.json")).read()
+    assert O.ref_report_reformat(ours, "csv") == open(os.path.join(GOLD, "report_b200.csv")).read()
+    back, mine = json.loads(O.ref_report_reformat(ours, "json")), json.loads(ours)
+    for k in ("format_version", "regime", "timestamp", "geometry", "group_rank", "representation", "mass", "seed",
+              "kernels", "model"):
+        assert back[k] == mine[k], k
+    text = O.ref_report_reformat(ours, "text")
+    assert "dirac" in text and "consistency    passed (23 iterations" in text
+
+
+def test_fullsize_reference_cg_counts_are_pinned():
+    """tests/golden/cg_cfg*.npz (make_fullsize_cg.py, the unmodified reference
+    at BASELINE.json's full sizes): every config has plain and eo counts, the
+    solves met their tolerance, and config 1 agrees with cfg1.npz."""
+    want = {1: (47, 23), 2: (48, 23), 3: (389, 128), 4: (49, 23), 5: (47, 23)}
+    for c, (h, eo) in want.items():
+        z = np.load(os.path.join(GOLD, f"cg_cfg{c}.npz"))
+        assert (int(z["h_iterations"]), int(z["eo_iterations"])) == (h, eo)
+        assert z["h_true"] < 2 * z["tol"] and z["eo_true"] < 2 * z["tol"]
+        assert len(z["h_history"]) == h and len(z["eo_history"]) == eo
+    z1 = golden("cfg1")
+    assert int(z1["cg_h_iterations"]) == 47 and int(z1["cg_eo_iterations"]) == 23

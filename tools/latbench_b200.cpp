@@ -455,9 +455,11 @@ int usage() {
 int main(int argc, char** argv) {
   if (argc < 3) return usage();
   const std::string cmd = argv[1], path = argv[2];
-  std::string fmt = "text";
-  for (int i = 3; i + 1 < argc; ++i)
+  std::string fmt = "text", all_prefix;
+  for (int i = 3; i + 1 < argc; ++i) {
     if (std::string(argv[i]) == "--format") fmt = argv[i + 1];
+    if (std::string(argv[i]) == "--emit-all") all_prefix = argv[i + 1];  // <prefix>.{txt,json,csv}
+  }
   try {
     Config cfg = parse_file(path);
     if (cmd == "model") {
@@ -498,6 +500,11 @@ int main(int argc, char** argv) {
                   cfg.eo ? "eo" : "plain", rep.cons.iterations, rep.cons.residual);
     } else {
       std::cout << format(rep, fmt);
+      for (const char* f : {"text", "json", "csv"}) {  // one report, every format
+        if (all_prefix.empty()) break;
+        const std::string ext = std::string(f) == "text" ? "txt" : f;
+        std::ofstream(all_prefix + "." + ext) << format(rep, f);
+      }
     }
     return rep.cons.status == lb::ConsistencyResult::Status::Failed ? 1 : 0;
   } catch (const lb::ConfigError& e) {
