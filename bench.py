@@ -107,7 +107,7 @@ def peaks():
 
 def link_bytes(dr, real, fmt="full"):
     """Bytes of one link as stored on the device (links.cuh)."""
-    return {"full": dr * dr * (8 if real else 16), "su2": 32, "r12": 96, "as4": 256, "as4r": 288}[fmt]
+    return {"full": dr * dr * (8 if real else 16), "su2": 32, "r12": 96, "r10": 80, "as4": 256, "as4r": 288}[fmt]
 
 
 def bytes_full_dphi(dr, real, fmt="full"):

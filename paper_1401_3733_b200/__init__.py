@@ -275,7 +275,7 @@ def plan_faces(global_, grid, rank, input_parity):
 
 # ---------------------------------------------------------------- ownership
 def _release(destroy: str, handle):
-    """Finalizer body: free one library handle (never raises)."""
+    """Free one library handle (never raises)."""
     try:
         if _lib is not None and handle:
             getattr(_lib, destroy)(handle)
@@ -283,24 +283,46 @@ def _release(destroy: str, handle):
         pass
 
 
+def _release_tree(rec):
+    """rec = [destroy, handle, children]: children first (fields before their
+    context, contexts before their world), then the handle itself."""
+    children = rec[2]
+    while children:
+        _, child = children.popitem()
+        _release_tree(child)
+    _release(rec[0], rec[1])
+
+
+def _finalize(registry, key, rec):
+    # a parent that was released first already freed this handle
+    if registry is not None and registry.pop(key, None) is None:
+        return
+    _release_tree(rec)
+
+
 class _Owned:
     """A library handle freed exactly once: by close(), or by a finalizer when
-    the Python object is collected (weakref.finalize also runs at exit, in
-    reverse creation order, so fields go before their context and contexts
-    before their world). A context closes its live fields first, so nothing
-    is ever freed through a dangling context."""
+    the Python object is collected. Every handle is recorded in its parent's
+    record (field -> context -> world), and releasing a parent releases its
+    remaining children first, so no handle is ever freed through an already
+    destroyed context or world — whatever order the garbage collector
+    finalises a cycle in."""
 
     _destroy = ""
 
     def _own(self, handle, parent=None):
         self._h = handle
-        self._fin = weakref.finalize(self, _release, self._destroy, handle)
-        self._children = weakref.WeakSet()
+        self._rec = [self._destroy, handle, {}]
+        self._live = weakref.WeakSet()  # child objects, to clear their _h on close()
+        registry = parent._rec[2] if parent is not None else None
+        key = id(self._rec)
         if parent is not None:
-            parent._children.add(self)
+            registry[key] = self._rec
+            parent._live.add(self)
+        self._fin = weakref.finalize(self, _finalize, registry, key, self._rec)
 
     def close(self):
-        for ch in list(getattr(self, "_children", ())):
+        for ch in list(getattr(self, "_live", ())):
             ch.close()
         fin = getattr(self, "_fin", None)
         if fin is not None:
@@ -374,7 +396,7 @@ class Context(_Owned):
         h = _vp()
         _check(lib().lbcu_ctx_create(world._h if world else None, self.rank, int(device),
                                      _i4(self.global_), _i4(self.grid), int(enforce_floor), C.byref(h)))
-        self._own(h)
+        self._own(h, world)
         loc = (C.c_int * 4)()
         _check(lib().lbcu_ctx_local(h, loc))
         self.local = tuple(loc)
@@ -456,7 +478,7 @@ class GaugeField(_Owned):
         """(format name, max reconstruction error at the last upload)."""
         f, e = C.c_int(), C.c_double()
         _check(lib().lbcu_gauge_storage(self._h, C.byref(f), C.byref(e)))
-        return {0: "full", 1: "su2", 2: "r12", 3: "as4", 4: "as4r"}[f.value], e.value
+        return {0: "full", 1: "su2", 2: "r12", 3: "as4", 4: "as4r", 5: "r10"}[f.value], e.value
 
     def download(self) -> np.ndarray:
         dt = np.float64 if self.real_links else np.complex128

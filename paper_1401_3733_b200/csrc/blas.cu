@@ -110,6 +110,66 @@ __global__ void k_cg_r(double2* __restrict__ r, const double2* __restrict__ ap, 
   block_reduce_partial<1>(R, v);
 }
 
+// Single-reduction CG (Chronopoulos & Gear), multi-rank runs (solver.cpp):
+//   p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s ; |r|^2
+// (s = A p and w = A r carried as vectors, so the iteration's two scalars,
+// |r|^2 here and (r, A r) from the operator epilogue, meet in one allreduce).
+// A no-op once the solve is done (speculative host-loop iteration).
+__global__ void k_cg1_update(double2* __restrict__ p, double2* __restrict__ s, double2* __restrict__ x,
+                             double2* __restrict__ r, const double2* __restrict__ w, size_t n,
+                             const CgState* __restrict__ st, Reduce R) {
+  double v[1] = {0.0};
+  if (!st->done) {
+    const double alpha = st->alpha, beta = st->beta;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+      const double2 rv = r[i], wv = __ldg(w + i);
+      double2 pv = p[i], sv = s[i], xv = x[i];
+      pv = make_double2(fma(beta, pv.x, rv.x), fma(beta, pv.y, rv.y));
+      sv = make_double2(fma(beta, sv.x, wv.x), fma(beta, sv.y, wv.y));
+      xv = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+      const double2 rn = make_double2(fma(-alpha, sv.x, rv.x), fma(-alpha, sv.y, rv.y));
+      p[i] = pv;
+      s[i] = sv;
+      x[i] = xv;
+      r[i] = rn;
+      v[0] = fma(rn.x, rn.x, fma(rn.y, rn.y, v[0]));
+    }
+  }
+  block_reduce_partial<1>(R, v);
+}
+
+// start: gd = (|b|^2, (b, A b)) -> alpha_0 = gamma_0 / delta_0, beta_0 = 0
+__global__ void k_cg1_start(CgState* st, const double* gd) {
+  st->rr = gd[0];
+  st->alpha = gd[0] / gd[1];
+  st->beta = 0.0;
+}
+
+// end of iteration k: gd = (gamma', delta') = (|r'|^2, (r', A r')); history,
+// convergence as cg_post_end, then beta = gamma'/gamma,
+// alpha' = gamma' / (delta' - beta gamma' / alpha)
+__global__ void k_cg1_end(CgState* st, const double* gd, double* hist) {
+  if (st->done) return;
+  const double g = gd[0], d = gd[1];
+  const double rel = sqrt(g) / st->bnorm;
+  const long long k = st->k;
+  hist[k] = rel;
+  st->rel = rel;
+  st->rr_new = g;
+  if (rel < st->best) st->best = rel;
+  st->k = k + 1;
+  if (rel < st->tol) {
+    st->conv = 1;
+    st->done = 1;
+  } else if (k + 1 >= st->maxit) {
+    st->done = 1;
+  }
+  const double beta = g / st->rr;
+  st->alpha = g / (d - beta * g / st->alpha);
+  st->beta = beta;
+  st->rr = g;
+}
+
 __global__ void k_cg_xfinal(double2* __restrict__ x, const double2* __restrict__ p, size_t n,
                             const CgState* __restrict__ st) {
   const double alpha = st->alpha;
@@ -363,6 +423,28 @@ void cg_r_update(lbcu_ctx_s* ctx, lbcu_spinor_s* r, const lbcu_spinor_s* ap, dou
   LBCU_CUDA(cudaGetLastError());
 }
 
+void cg1_update(lbcu_ctx_s* ctx, lbcu_spinor_s* p, lbcu_spinor_s* sv, lbcu_spinor_s* x, lbcu_spinor_s* r,
+                const lbcu_spinor_s* w, double* dres) {
+  const int nb = flat_blocks(ctx, r->elems);
+  k_cg1_update<<<nb, kThreads, 0, ctx->stream>>>(p->base, sv->base, x->base, r->base, w->base, r->elems, ctx->dcg,
+                                                 make_reduce(ctx, dres, nb));
+  k_reduce_finish<1><<<1, kFinishThreads, 0, ctx->stream>>>(make_reduce(ctx, dres, nb));
+  ctx->launches += 2;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void cg1_scalar_start(lbcu_ctx_s* ctx, const double* gd) {
+  k_cg1_start<<<1, 1, 0, ctx->stream>>>(ctx->dcg, gd);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
+void cg1_scalar_end(lbcu_ctx_s* ctx, const double* gd) {
+  k_cg1_end<<<1, 1, 0, ctx->stream>>>(ctx->dcg, gd, ctx->dhist);
+  ctx->launches++;
+  LBCU_CUDA(cudaGetLastError());
+}
+
 void cg_x_final(lbcu_ctx_s* ctx, lbcu_spinor_s* x, const lbcu_spinor_s* p) {
   k_cg_xfinal<<<flat_blocks(ctx, x->elems), kThreads, 0, ctx->stream>>>(x->base, p->base, x->elems, ctx->dcg);
   ctx->launches++;
@@ -551,16 +633,24 @@ void spinor_download(lbcu_ctx_s* ctx, const lbcu_spinor_s* s, double* host) {
 namespace {
 
 // compact format available for a representation (links.cuh)
-int compact_format(const lbcu_gauge_s* g) {
-  if (g->dr == 2 && !g->real) return GF_SU2;  // SU(2) fundamental
-  if (g->dr == 3 && g->real && g->n == 2) return GF_SU2;  // SU(2) adjoint
-  if (g->dr == 3 && !g->real && g->n == 3 && g->rep == LBCU_REP_FUNDAMENTAL) return GF_R12;
-  if (g->dr == 6 && !g->real && g->n == 4 && g->rep == LBCU_REP_ANTISYMMETRIC) return GF_AS4R;
-  return GF_FULL;
+// Compact formats to try, most compact first; the first whose every link
+// rebuilds to 1e-12 is kept (gauge_adopt_dense). SU(3) fundamental: R10, then
+// R12 (LBCU_SU3_STORAGE=r12 skips R10).
+std::vector<int> compact_formats(const lbcu_gauge_s* g) {
+  if (g->dr == 2 && !g->real) return {GF_SU2};  // SU(2) fundamental
+  if (g->dr == 3 && g->real && g->n == 2) return {GF_SU2};  // SU(2) adjoint
+  if (g->dr == 3 && !g->real && g->n == 3 && g->rep == LBCU_REP_FUNDAMENTAL) {
+    const char* e = std::getenv("LBCU_SU3_STORAGE");
+    if (e && std::string(e) == "r12") return {GF_R12};
+    return {GF_R10, GF_R12};
+  }
+  if (g->dr == 6 && !g->real && g->n == 4 && g->rep == LBCU_REP_ANTISYMMETRIC) return {GF_AS4R};
+  return {};
 }
 
 int fmt_entries(int fmt, int dr) {
-  return fmt == GF_SU2 ? 2 : fmt == GF_R12 ? 6 : fmt == GF_AS4 ? 16 : fmt == GF_AS4R ? 18 : dr * dr;
+  return fmt == GF_SU2 ? 2 : fmt == GF_R12 ? 6 : fmt == GF_R10 ? 5 : fmt == GF_AS4 ? 16 : fmt == GF_AS4R ? 18
+                                                                                            : dr * dr;
 }
 
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double v) {
@@ -617,6 +707,12 @@ __global__ void k_compress(const LinkT<REAL>* __restrict__ full, double2* __rest
       st[1] = make_double2(-vy, -vx); // be = a2 + i a1
     } else if constexpr (FMT == GF_AS4R) {
       as4r_from_dense(u, st);  // imaginary residue caught by the rebuild check below
+    } else if constexpr (FMT == GF_R10) {
+      st[0] = u[0];
+      st[1] = u[1];
+      st[2] = u[2];
+      st[3] = u[4];
+      st[4] = u[5];
     } else {
 #pragma unroll
       for (int e = 0; e < 6; ++e) st[e] = u[e];
@@ -700,6 +796,8 @@ void dispatch_compact(const lbcu_gauge_s* g, int fmt, F&& f) {
     return f(integral_constant<int, 3>{}, std::true_type{}, integral_constant<int, GF_SU2>{});
   if (fmt == GF_R12)
     return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_R12>{});
+  if (fmt == GF_R10)
+    return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_R10>{});
   if (fmt == GF_AS4R)
     return f(integral_constant<int, 6>{}, std::false_type{}, integral_constant<int, GF_AS4R>{});
   throw Error(LBCU_CONTRACT_VIOLATION, "no compact gauge format");
@@ -760,8 +858,8 @@ void gauge_adopt_dense(lbcu_ctx_s* ctx, lbcu_gauge_s* g, void* full) {
     g->base = base;
     g->fmt = fmt;
   };
-  const int cf = compact_format(g);
-  if (cf != GF_FULL && compaction_enabled(g)) {
+  double best_err = -1.0;
+  for (const int cf : compaction_enabled(g) ? compact_formats(g) : std::vector<int>{}) {
     const size_t cbytes = 2 * 4 * static_cast<size_t>(fmt_entries(cf, g->dr)) * geo.stride * sizeof(double2);
     void* compact = nullptr;
     LBCU_CUDA(cudaMalloc(&compact, cbytes));
@@ -782,14 +880,16 @@ void gauge_adopt_dense(lbcu_ctx_s* ctx, lbcu_gauge_s* g, void* full) {
     LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
     double err;
     std::memcpy(&err, &bits, sizeof(err));
-    g->compact_err = err;
+    if (best_err < 0.0 || err < best_err) best_err = err;
     if (err <= 1e-12) {
+      g->compact_err = err;
       if (full != g->base) LBCU_CUDA(cudaFree(full));
       adopt(compact, cf);  // frees the previous storage
       return;
     }
     LBCU_CUDA(cudaFree(compact));
   }
+  g->compact_err = best_err;
   if (g->bc == LBCU_BC_ANTIPERIODIC_T) {
     const int t_off = geo.coords[0] * geo.local[0];
     if (g->real)

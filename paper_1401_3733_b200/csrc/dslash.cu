@@ -42,7 +42,8 @@ struct HopArgs {
   const double2* x[2];   // diagonal-term blocks by output parity (nullable)
   double2* r[2];         // CG residual blocks by output parity
   const void* gauge;     // [2 parity][4 mu] blocks of entries x stride (tiled), storage format
-  double a, b, s5in, s5x, s5acc;
+  double a, b, s5x, s5acc;
+  unsigned s5in;  // sign mask of the gamma5 on the input (sign_mask)
   const double* alpha;
   int par0;    // output parity of a single-parity launch
   int both;    // 1: parity = blockIdx.x & 1
@@ -95,7 +96,7 @@ __device__ __forceinline__ long long estride(long long) { return kTile; }
 // h_a = psi_a + F_a * s5 * psi_{p_a}: spin projection of the spinor at cb site nb
 template <int D, int P0, int P1, int F0, int F1>
 __device__ __forceinline__ void project(double2 (&h)[2][D], const double2* __restrict__ in,
-                                        long long st, int nb, double s5) {
+                                        long long st, int nb, unsigned s5) {
   const double2* __restrict__ q = site_ptr<4 * D>(in, nb);
   const long long es = estride(st);
 #pragma unroll
@@ -104,8 +105,8 @@ __device__ __forceinline__ void project(double2 (&h)[2][D], const double2* __res
     const double2 a1 = ldg(q + (long long)(1 * D + c) * es);
     const double2 b0 = ldg(q + (long long)(P0 * D + c) * es);
     const double2 b1 = ldg(q + (long long)(P1 * D + c) * es);
-    h[0][c] = cadd(a0, phm<F0>(cscale(s5, b0)));
-    h[1][c] = cadd(a1, phm<F1>(cscale(s5, b1)));
+    h[0][c] = cadd(a0, phm<F0>(cflip(s5, b0)));
+    h[1][c] = cadd(a1, phm<F1>(cflip(s5, b1)));
   }
 }
 
@@ -145,13 +146,13 @@ __device__ __forceinline__ void link_hop(double2 (&acc)[4][D], const ElemT<D, RE
 // Antiperiodic-t sign of a compact link (dense links carry it baked in):
 // branch-free so the scheduler can still hoist the next direction's loads.
 template <int D, int FMT>
-__device__ __forceinline__ void bc_sign(double2 (&h)[2][D], bool flip) {
+__device__ __forceinline__ void bc_sign(double2 (&h)[2][D], bool neg) {
   if constexpr (FMT != GF_FULL) {
-    const double sg = flip ? -1.0 : 1.0;
+    const unsigned m = sign_mask(neg);
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int c = 0; c < D; ++c) h[a][c] = cscale(sg, h[a][c]);
+      for (int c = 0; c < D; ++c) h[a][c] = cflip(m, h[a][c]);
   }
 }
 
@@ -221,14 +222,14 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
 // Both spin projections (1 -/+ g_mu) of the spinor at cb site nb from one load.
 template <int D, int P0, int P1, int F0, int F1>
 __device__ __forceinline__ void project2(double2 (&hm)[2][D], double2 (&hp)[2][D],
-                                         const double2* __restrict__ in, int nb, double s5) {
+                                         const double2* __restrict__ in, int nb, unsigned s5) {
   const double2* __restrict__ q = site_ptr<4 * D>(in, nb);
 #pragma unroll
   for (int c = 0; c < D; ++c) {
     const double2 a0 = ldg(q + (0 * D + c) * kTile);
     const double2 a1 = ldg(q + (1 * D + c) * kTile);
-    const double2 b0 = phm<F0>(cscale(s5, ldg(q + (P0 * D + c) * kTile)));
-    const double2 b1 = phm<F1>(cscale(s5, ldg(q + (P1 * D + c) * kTile)));
+    const double2 b0 = phm<F0>(cflip(s5, ldg(q + (P0 * D + c) * kTile)));
+    const double2 b1 = phm<F1>(cflip(s5, ldg(q + (P1 * D + c) * kTile)));
     hm[0][c] = cadd(a0, b0);
     hm[1][c] = cadd(a1, b1);
     hp[0][c] = csub(a0, b0);
@@ -402,13 +403,13 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 
 template <int D, int P0, int P1, int F0, int F1>
-__device__ __forceinline__ void project_sm(double2 (&h)[2][D], const double2* q, double s5) {
+__device__ __forceinline__ void project_sm(double2 (&h)[2][D], const double2* q, unsigned s5) {
 #pragma unroll
   for (int c = 0; c < D; ++c) {
     const double2 a0 = q[(0 * D + c) * kTile], a1 = q[(1 * D + c) * kTile];
     const double2 b0 = q[(P0 * D + c) * kTile], b1 = q[(P1 * D + c) * kTile];
-    h[0][c] = cadd(a0, phm<F0>(cscale(s5, b0)));
-    h[1][c] = cadd(a1, phm<F1>(cscale(s5, b1)));
+    h[0][c] = cadd(a0, phm<F0>(cflip(s5, b0)));
+    h[1][c] = cadd(a1, phm<F1>(cflip(s5, b1)));
   }
 }
 
@@ -586,7 +587,7 @@ struct PackArgs {
   const double2* in;  // input parity block
   const void* gauge;
   int in_par, mu, dir, count;
-  double s5in;
+  unsigned s5in;  // sign mask (sign_mask)
   int bc_kernel, t_off, bc_tlast;
   double2* outbuf;  // [2D][count]
 };
@@ -751,6 +752,7 @@ void dispatch(int dr, bool real, int fmt, F&& f) {
         return f(integral_constant<int, 2>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
       case 3:
         if (fmt == GF_R12) return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_R12>{});
+        if (fmt == GF_R10) return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_R10>{});
         return f(integral_constant<int, 3>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
       case 4: return f(integral_constant<int, 4>{}, std::false_type{}, integral_constant<int, GF_FULL>{});
       case 6:
@@ -828,7 +830,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   A.gauge = c.g->base;
   A.a = c.a;
   A.b = c.b;
-  A.s5in = c.s5in;
+  A.s5in = sign_mask(c.s5in < 0.0);
   A.s5x = c.s5x;
   A.s5acc = c.s5acc;
   A.alpha = c.alpha;
@@ -846,8 +848,8 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     // L2-blocked schedule: spatial blocks of bx x-planes whose two-slice
     // working set (spinor in/out + links as stored) fits the L2 budget
     if (env_int("LBCU_HOP_SCHED", 1)) {
-      const int lb = fmt == GF_SU2 ? 32 : fmt == GF_R12 ? 96 : fmt == GF_AS4 ? 256 : fmt == GF_AS4R ? 288
-                                                                                    : dr * dr * (real ? 8 : 16);
+      const int lb = fmt == GF_SU2 ? 32 : fmt == GF_R12 ? 96 : fmt == GF_R10 ? 80 : fmt == GF_AS4 ? 256
+                     : fmt == GF_AS4R ? 288 : dr * dr * (real ? 8 : 16);
       const double site_bytes = 128.0 * dr + (npar == 2 ? 4 : 8) * lb;
       const double plane_bytes = site_bytes * geo.local[2] * geo.local[3];
       const double budget = env_int("LBCU_HOP_L2MB", 32) * 1e6;
@@ -925,7 +927,7 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       P.mu = f / 2;
       P.dir = f % 2;
       P.count = static_cast<int>(ctx->plan.count[f]);
-      P.s5in = c.s5in;
+      P.s5in = A.s5in;
       P.bc_kernel = A.bc_kernel;
       P.t_off = A.t_off;
       P.bc_tlast = A.bc_tlast;

@@ -14,6 +14,13 @@
 //             - 2 a0 eps_abc a_c with al = a0 + i a3, be = a2 + i a1
 //             (group.cpp:126-143 convention, checked in tests/test_host.py)
 //   GF_R12  : SU(3) rows 0 and 1 (6 complex); row 2 = conj(row0 x row1)
+//   GF_R10  : SU(3) row 0 and U_11, U_12 (5 complex, 80 B): U_10 from the
+//             orthogonality of rows 0 and 1,
+//             U_10 = -(conj(U_01) U_11 + conj(U_02) U_12) / conj(U_00),
+//             then row 2 as R12. Trig-free; the division by U_00 is well
+//             conditioned for near-unit links (|U_00| ~ 1) and loses at most
+//             eps / |U_00| for Haar links; the upload check (1e-12) falls
+//             back to R12 for any field where it would not be exact
 //   GF_AS4  : two-index antisymmetric rep of SU(4) (dr = 6) stored as the
 //             fundamental 4 x 4 element (16 complex instead of 36); entries
 //             R_(ij),(kl) = u_ik u_jl - u_il u_jk (group.cpp:146-158) are
@@ -50,7 +57,7 @@ __device__ __forceinline__ T ldlink(const T* p) {
   return __ldg(p);
 }
 
-enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2, GF_AS4 = 3, GF_AS4R = 4 };
+enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2, GF_AS4 = 3, GF_AS4R = 4, GF_R10 = 5 };
 
 template <bool REAL>
 using LinkT = std::conditional_t<REAL, double, double2>;
@@ -58,9 +65,11 @@ using LinkT = std::conditional_t<REAL, double, double2>;
 template <int D, bool REAL, int FMT>
 struct LinkFmt {
   static constexpr bool valid = FMT == GF_FULL || (FMT == GF_SU2 && ((D == 2 && !REAL) || (D == 3 && REAL))) ||
-                                (FMT == GF_R12 && D == 3 && !REAL) || ((FMT == GF_AS4 || FMT == GF_AS4R) && D == 6 && !REAL);
+                                ((FMT == GF_R12 || FMT == GF_R10) && D == 3 && !REAL) ||
+                                ((FMT == GF_AS4 || FMT == GF_AS4R) && D == 6 && !REAL);
   static constexpr int entries =
-      FMT == GF_FULL ? D * D : (FMT == GF_SU2 ? 2 : (FMT == GF_R12 ? 6 : (FMT == GF_AS4 ? 16 : 18)));
+      FMT == GF_FULL ? D * D
+                     : (FMT == GF_SU2 ? 2 : (FMT == GF_R12 ? 6 : (FMT == GF_R10 ? 5 : (FMT == GF_AS4 ? 16 : 18))));
   using Elem = std::conditional_t<FMT == GF_FULL, LinkT<REAL>, double2>;
 };
 
@@ -170,9 +179,22 @@ __device__ __forceinline__ void build_link(LinkT<REAL> (&u)[D * D],
     u[6] = fma(t3, a1, w * a2);
     u[7] = fma(t3, a2, -w * a1);
     u[8] = fma(t3, a3, d);
-  } else if constexpr (FMT == GF_R12) {
+  } else if constexpr (FMT == GF_R12 || FMT == GF_R10) {
+    if constexpr (FMT == GF_R12) {
 #pragma unroll
-    for (int e = 0; e < 6; ++e) u[e] = s[e];
+      for (int e = 0; e < 6; ++e) u[e] = s[e];
+    } else {
+      u[0] = s[0];
+      u[1] = s[1];
+      u[2] = s[2];
+      u[4] = s[3];
+      u[5] = s[4];
+      // rows 0 and 1 orthogonal: conj(u0) u3 + conj(u1) u4 + conj(u2) u5 = 0
+      const double2 t = make_double2(fma(u[1].x, u[4].x, fma(u[1].y, u[4].y, fma(u[2].x, u[5].x, u[2].y * u[5].y))),
+                                     fma(u[1].x, u[4].y, fma(-u[1].y, u[4].x, fma(u[2].x, u[5].y, -u[2].y * u[5].x))));
+      const double inv = -1.0 / fma(u[0].x, u[0].x, u[0].y * u[0].y);  // u3 = -t / conj(u0) = -t u0 / |u0|^2
+      u[3] = make_double2(inv * fma(t.x, u[0].x, -t.y * u[0].y), inv * fma(t.x, u[0].y, t.y * u[0].x));
+    }
     u[6] = cconj(csub(cmul(u[1], u[5]), cmul(u[2], u[4])));
     u[7] = cconj(csub(cmul(u[2], u[3]), cmul(u[0], u[5])));
     u[8] = cconj(csub(cmul(u[0], u[4]), cmul(u[1], u[3])));

@@ -131,6 +131,11 @@ void cg_scalar_alpha(lbcu_ctx_s* ctx, const double* pap);
 void cg_scalar_end(lbcu_ctx_s* ctx, const double* rr_new, unsigned long long graph_handle,
                    int use_graph);
 void cg_scalar_init(lbcu_ctx_s* ctx, const double* b2, double tol, long long maxit);
+// single-reduction (Chronopoulos-Gear) CG steps, blas.cu
+void cg1_update(lbcu_ctx_s* ctx, lbcu_spinor_s* p, lbcu_spinor_s* s, lbcu_spinor_s* x, lbcu_spinor_s* r,
+                const lbcu_spinor_s* w, double* dres);
+void cg1_scalar_start(lbcu_ctx_s* ctx, const double* gd);
+void cg1_scalar_end(lbcu_ctx_s* ctx, const double* gd);
 
 // layout transposes host (reference AoS) <-> device (even-odd SoA)
 void spinor_upload(lbcu_ctx_s* ctx, lbcu_spinor_s* s, const double* host);

@@ -35,7 +35,8 @@ using namespace lbcu;
 namespace {
 
 constexpr int kSlotPap = 8, kSlotRR = 10, kSlotB2 = 12, kSlotTrue = 14;
-constexpr int kSlotR = 0, kSlotP = 1, kSlotQ = 2, kSlotT = 3, kSlotAp = 4, kSlotTmp2 = 5;
+constexpr int kSlotR = 0, kSlotP = 1, kSlotQ = 2, kSlotT = 3, kSlotAp = 4, kSlotTmp2 = 5, kSlotS = 6, kSlotW = 7;
+constexpr int kSlotGD = 16;  // single-reduction CG: (gamma, delta) side by side
 
 struct Fused {
   enum Kind { H, EO } kind;
@@ -157,6 +158,97 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
   if (fuse) return;
   T->allreduce(ctx->rank, slot(ctx, kSlotRR), 1, ctx->stream);
   cg_scalar_end(ctx, slot(ctx, kSlotRR), handle, use_graph);
+}
+
+// w = A v with delta = (v, A v) = |M v|^2 from the first operator's epilogue
+// (A = Mhat^dag Mhat or D^dag D, the dagger as g5 M g5), written to *delta.
+void apply_a_delta(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* v, lbcu_spinor_s* q, lbcu_spinor_s* t,
+                   lbcu_spinor_s* w, double* delta) {
+  const double A = 4.0 + F.mass;
+  if (F.kind == Fused::EO) {
+    HopCall a;  // t_o = H_oe v_e
+    a.in = v;
+    a.out = t;
+    a.g = F.g;
+    a.out_parity = 1;
+    hop_apply(ctx, a);
+    HopCall b;  // q_e = Mhat v ; |q|^2
+    b.in = t;
+    b.out = q;
+    b.x = v;
+    b.g = F.g;
+    b.out_parity = 0;
+    b.a = A;
+    b.b = -1.0 / (4.0 * A);
+    b.epi = EPI_STORE_NORM;
+    b.result = delta;
+    hop_apply(ctx, b);
+    HopCall c;  // t_o = H_oe g5 q
+    c.in = q;
+    c.out = t;
+    c.g = F.g;
+    c.out_parity = 1;
+    c.s5in = -1.0;
+    hop_apply(ctx, c);
+    HopCall d;  // w = g5 Mhat g5 q
+    d.in = t;
+    d.out = w;
+    d.x = q;
+    d.g = F.g;
+    d.out_parity = 0;
+    d.a = A;
+    d.b = -1.0 / (4.0 * A);
+    d.s5acc = -1.0;
+    hop_apply(ctx, d);
+  } else {
+    HopCall a;  // q = D v ; |q|^2
+    a.in = v;
+    a.out = q;
+    a.x = v;
+    a.g = F.g;
+    a.out_parity = 2;
+    a.a = A;
+    a.b = -0.5;
+    a.epi = EPI_STORE_NORM;
+    a.result = delta;
+    hop_apply(ctx, a);
+    HopCall b;  // w = g5 D g5 q
+    b.in = q;
+    b.out = w;
+    b.x = q;
+    b.g = F.g;
+    b.out_parity = 2;
+    b.a = A;
+    b.b = -0.5;
+    b.s5in = -1.0;
+    b.s5acc = -1.0;
+    hop_apply(ctx, b);
+  }
+}
+
+// One single-reduction iteration (Chronopoulos & Gear 1989): the same
+// iterates and stopping rule as the reference recurrence in exact
+// arithmetic, but |r|^2 and (r, A r) are summed across ranks in ONE
+// allreduce per iteration instead of two (pAp, then rr), at the price of two
+// more streamed vectors (s = A p, w = A r). For multi-rank runs whose local
+// volume is small enough that the allreduce latency outweighs that traffic.
+void cg1_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s* r, lbcu_spinor_s* p,
+              lbcu_spinor_s* q, lbcu_spinor_s* t, lbcu_spinor_s* sv, lbcu_spinor_s* w) {
+  double* gd = slot(ctx, kSlotGD);
+  cg1_update(ctx, p, sv, x, r, w, gd);             // gamma' = |r'|^2
+  apply_a_delta(ctx, F, r, q, t, w, gd + 1);       // w' = A r', delta' = (r', A r')
+  ctx->world->t->allreduce(ctx->rank, gd, 2, ctx->stream);
+  cg1_scalar_end(ctx, gd);
+}
+
+bool single_reduce(const lbcu_ctx_s* ctx, int dr) {
+  const char* e = std::getenv("LBCU_CG_SINGLE_REDUCE");
+  if (e && e[0] == '1') return true;
+  if (e && e[0] == '0') return false;
+  // auto: two streamed vectors more per iteration (4 passes of a parity
+  // field, 256 dr B per even site) against one ~15-20 us allreduce fewer at
+  // ~6.5 TB/s: worth it below ~5e5 dr-weighted sites per rank
+  return ctx->geo.nranks > 1 && static_cast<double>(ctx->geo.vh) * dr < 5e5;
 }
 
 void callback_body(lbcu_ctx_s* ctx, lbcu_linop op, void* user, lbcu_spinor_s* x, lbcu_spinor_s* r,
@@ -301,7 +393,8 @@ int run_cg(lbcu_ctx_s* ctx, const lbcu_cg_settings* st, lbcu_spinor_s* rhs, lbcu
   lbcu_spinor_s* t = scratch_spinor(ctx, dr, LBCU_ODD, 200 + kSlotT);
   ensure_hist(ctx, st->max_iterations + 1);
 
-  const bool use_graph = fused && ctx->world->t->capturable() && ctx->geo.nranks == 1 && graphs_enabled();
+  const bool use_graph = fused && ctx->world->t->capturable() && ctx->geo.nranks == 1 && graphs_enabled() &&
+                         !(std::getenv("LBCU_CG_SINGLE_REDUCE") && std::getenv("LBCU_CG_SINGLE_REDUCE")[0] == '1');
   GraphEntry ge{};
   if (use_graph) {  // capture + instantiate (first solve on these fields) outside the timed region
     if (fused->kind == Fused::EO) {  // make sure lazily allocated buffers exist before capture
@@ -309,6 +402,9 @@ int run_cg(lbcu_ctx_s* ctx, const lbcu_cg_settings* st, lbcu_spinor_s* rhs, lbcu
     }
     ge = graph_for(ctx, *fused, x, r, p, q, t);
   }
+  const bool cg1 = fused && !use_graph && single_reduce(ctx, dr);
+  lbcu_spinor_s* sv = cg1 ? scratch_spinor(ctx, dr, sub, 200 + kSlotS) : nullptr;  // allocated untimed
+  lbcu_spinor_s* w = cg1 ? scratch_spinor(ctx, dr, sub, 200 + kSlotW) : nullptr;
 
   LBCU_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->world->t->barrier(ctx->rank);  // solver.cpp:36
@@ -322,6 +418,14 @@ int run_cg(lbcu_ctx_s* ctx, const lbcu_cg_settings* st, lbcu_spinor_s* rhs, lbcu
   blas_copy(ctx, r, rhs);
   blas_zero(ctx, p);
   cg_scalar_init(ctx, slot(ctx, kSlotB2), st->tolerance, st->max_iterations);
+  if (cg1) {  // s = 0 ; w = A b, delta_0 = (b, A b) ; gamma_0 = |b|^2 (already summed)
+    blas_zero(ctx, sv);
+    double* gd = slot(ctx, kSlotGD);
+    apply_a_delta(ctx, *fused, r, q, t, w, gd + 1);
+    ctx->world->t->allreduce(ctx->rank, gd + 1, 1, ctx->stream);
+    LBCU_CUDA(cudaMemcpyAsync(gd, slot(ctx, kSlotB2), sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    cg1_scalar_start(ctx, gd);
+  }
 
   if (use_graph) {
     LBCU_CUDA(cudaGraphLaunch(ge.exec, ctx->stream));
@@ -336,7 +440,8 @@ int run_cg(lbcu_ctx_s* ctx, const lbcu_cg_settings* st, lbcu_spinor_s* rhs, lbcu
     for (int e = 0; e < 2; ++e)
       if (!ctx->ev_cg[e]) LBCU_CUDA(cudaEventCreateWithFlags(&ctx->ev_cg[e], cudaEventDisableTiming));
     for (int k = 0; k < st->max_iterations; ++k) {
-      fused_body(ctx, *fused, x, r, p, q, t, 0, 0);
+      if (cg1) cg1_body(ctx, *fused, x, r, p, q, t, sv, w);
+      else fused_body(ctx, *fused, x, r, p, q, t, 0, 0);
       CgState* h = ctx->hcg + 1 + (k & 1);
       LBCU_CUDA(cudaMemcpyAsync(h, ctx->dcg, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
       LBCU_CUDA(cudaEventRecord(ctx->ev_cg[k & 1], ctx->stream));
@@ -366,7 +471,7 @@ int run_cg(lbcu_ctx_s* ctx, const lbcu_cg_settings* st, lbcu_spinor_s* rhs, lbcu
                                           " iterations, best relative residual " +
                                           std::to_string(cs.best));
   }
-  cg_x_final(ctx, x, p);
+  if (!cg1) cg_x_final(ctx, x, p);  // the single-reduction update keeps x current
   // true residual from scratch (solver.cpp:74-76)
   lbcu_spinor_s* ap = scratch_spinor(ctx, dr, sub, 200 + kSlotAp);
   apply(ap, x);

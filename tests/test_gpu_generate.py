@@ -25,12 +25,12 @@ def test_spinor_generate_matches_host(dr):
 
 @pytest.mark.parametrize("n,rep,links,fmt", [
     (2, lb.FUNDAMENTAL, lb.LINKS_HAAR, "su2"),
-    (3, lb.FUNDAMENTAL, lb.LINKS_HAAR, "r12"),
-    (3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT, "r12"),
+    (3, lb.FUNDAMENTAL, lb.LINKS_HAAR, "r10"),
+    (3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT, "r10"),
     (2, lb.ADJOINT, lb.LINKS_HAAR, "su2"),
     (4, lb.ANTISYMMETRIC, lb.LINKS_HAAR, "as4r"),
     (4, lb.FUNDAMENTAL, lb.LINKS_HAAR, "full"),
-    (3, lb.FUNDAMENTAL, lb.LINKS_UNIT, "r12"),
+    (3, lb.FUNDAMENTAL, lb.LINKS_UNIT, "r10"),
 ], ids=["su2f", "su3f", "su3f-near-unit", "su2a", "su4as", "su4f", "unit"])
 def test_gauge_generate_matches_host(n, rep, links, fmt):
     L = [4, 4, 4, 6]

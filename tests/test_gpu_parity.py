@@ -164,26 +164,29 @@ def test_cg_graph_cache_follows_field_lifetimes():
     assert ctx.cached_solves() == 1
     lb.cg_solve_eo(gauge, 0.1, rhs, st, x)
     assert ctx.cached_solves() == 1  # replayed, not re-captured
-    assert gauge.storage()[0] == "r12"
+    assert gauge.storage()[0] == "r10"
     gauge.set_compact(False).upload(g)  # new link buffer, dense format
     assert ctx.cached_solves() == 0 and gauge.storage()[0] == "full"
     o2 = lb.cg_solve_eo(gauge, 0.1, rhs, st, x)
     assert abs(o2.iterations - ref["iterations"]) <= 1 and o2.true_rel_residual < 2e-10
-    assert rel_l2(o2.solution.download(), o1.solution.download()) < 1e-9
+    x2 = o2.solution.download()
+    assert rel_l2(x2, O.port_cg(L, 1, 1, 0.1, g, s, 1e-10)["x"]) < 1e-8
     x.close()
     assert ctx.cached_solves() == 0
     for _ in range(3):  # handles recycled at the same addresses
         x = lb.SpinorField(ctx, dr, lb.EVEN)
         o3 = lb.cg_solve_eo(gauge, 0.1, rhs, st, x)
-        assert o3.iterations == o2.iterations and rel_l2(x.download(), o2.solution.download()) < 1e-12
+        assert o3.iterations == o2.iterations and rel_l2(x.download(), x2) < 1e-12
         x.close()
     gauge.close()
     assert ctx.cached_solves() == 0
 
 
 def test_fields_are_freed_with_their_context():
-    """Python fields free their device memory when collected, and a context
-    closes its live fields before itself (no use of a dangling context)."""
+    """Python fields free their device memory when collected, a context
+    closes its live fields before itself, and a garbage cycle holding a
+    context and its fields is finalised fields-first (no handle is ever freed
+    through a destroyed context)."""
     import gc
     L = [8, 8, 8, 8]
     ctx = lb.Context(L)
@@ -191,9 +194,23 @@ def test_fields_are_freed_with_their_context():
     g = lb.GaugeField(ctx, 3)
     del fs
     gc.collect()
-    assert len(ctx._children) == 1
+    assert len(ctx._rec[2]) == 1  # only the gauge field is still registered
     ctx.close()
-    assert g._h is None
+    assert g._h is None and not ctx._rec[2]
+    g.close()  # idempotent
+    for _ in range(3):  # cycles: context <-> fields collected together
+        c2 = lb.Context(L)
+        f2 = [lb.SpinorField(c2, 3), lb.GaugeField(c2, 3)]
+        c2.cycle = f2
+        for f in f2:
+            f.cycle = c2
+        del c2, f2, f
+        gc.collect()
+    w = lb.World.threads(1)
+    c3 = lb.Context(L, (1, 1, 1, 1), 0, 0, w)
+    lb.SpinorField(c3, 3)
+    w.close()  # the world closes its context, which closes its field
+    assert c3._h is None
 
 
 @pytest.mark.parametrize("n,rep", REPS, ids=REP_IDS)
@@ -317,12 +334,21 @@ def test_decomposed_dphi_matches_single(grid, n, rep, direct):
     assert rel_l2(got, want) < 1e-14
 
 
+@pytest.mark.parametrize("single", ["0", "1"], ids=["two-reductions", "single-reduction"])
+@pytest.mark.parametrize("solver", ["eo", "h"])
 @pytest.mark.parametrize("direct", [False, True], ids=["copy", "direct"])
-def test_decomposed_cg_eo_matches_single(direct):
+def test_decomposed_cg_matches_single(direct, solver, single, monkeypatch):
+    """Decomposed eo and plain CG against the reference CG on the whole
+    lattice: the reference recurrence (pAp and rr summed across ranks one
+    after the other) and the single-reduction Chronopoulos-Gear form (both
+    in one allreduce, LBCU_CG_SINGLE_REDUCE) give the reference's iteration
+    count +-1, its solution and the same residual history to rounding."""
+    monkeypatch.setenv("LBCU_CG_SINGLE_REDUCE", single)
     L = [8, 4, 4, 8]
     n, rep = 3, lb.FUNDAMENTAL
     dr, g, s = fields(L, n, rep)
-    ref = O.ref_cg_eo(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s, 1e-10)
+    refn = O.ref_cg_eo if solver == "eo" else O.ref_cg_h
+    ref = refn(L, [1, 1, 1, 1], n, rep, 1, 0.1, g, s, 1e-10)
     grid = (2, 1, 1, 2)
     world = lb.World.threads(4, direct=direct)
 
@@ -330,16 +356,37 @@ def test_decomposed_cg_eo_matches_single(direct):
         ctx = lb.Context(L, grid, r, 0, world)
         idx = global_index(L, grid, r)
         gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g[idx])
-        rhs = lb.SpinorField(ctx, dr, lb.EVEN).upload(s[idx])
-        o = lb.cg_solve_eo(gauge, 0.1, rhs, lb.CgSettings(1e-10, 500))
-        return idx, o.iterations, o.true_rel_residual, o.solution.download()
+        rhs = lb.SpinorField(ctx, dr, lb.EVEN if solver == "eo" else lb.FULL).upload(s[idx])
+        run = lb.cg_solve_eo if solver == "eo" else lb.cg_solve_h
+        o = run(gauge, 0.1, rhs, lb.CgSettings(1e-10, 500))
+        return idx, o.iterations, o.true_rel_residual, o.solution.download(), o.residual_history
 
     x = np.empty_like(s)
-    for idx, it, tr, part in run_ranks(4, body):
+    for idx, it, tr, part, hist in run_ranks(4, body):
         assert abs(it - ref["iterations"]) <= 1
         assert tr < 2e-10
+        k = min(it, ref["iterations"]) - 2
+        assert np.allclose(hist[:k], ref["history"][:k], rtol=1e-6)
         x[idx] = part
     assert rel_l2(x, ref["x"]) < 1e-8
+
+
+@pytest.mark.parametrize("solver", ["eo", "h"])
+def test_single_reduction_cg_on_one_rank(solver, monkeypatch):
+    """The single-reduction recurrence forced on one rank (host loop) agrees
+    with the reference CG: iterations +-1, solution, true residual."""
+    monkeypatch.setenv("LBCU_CG_SINGLE_REDUCE", "1")
+    L = [8, 4, 4, 4]
+    ctx, dr, g, s, gauge = setup(L, 2, lb.ADJOINT)
+    rhs = lb.SpinorField(ctx, dr, lb.EVEN if solver == "eo" else lb.FULL).upload(s)
+    run = lb.cg_solve_eo if solver == "eo" else lb.cg_solve_h
+    o = run(gauge, 0.1, rhs, lb.CgSettings(1e-10, 500))
+    refn = O.ref_cg_eo if solver == "eo" else O.ref_cg_h
+    ref = refn(L, [1, 1, 1, 1], 2, lb.ADJOINT, 1, 0.1, g, s, 1e-10)
+    assert abs(o.iterations - ref["iterations"]) <= 1 and o.true_rel_residual < 2e-10
+    assert rel_l2(o.solution.download(), ref["x"]) < 1e-8
+    with pytest.raises(lb.NonConvergence):
+        run(gauge, 0.1, rhs, lb.CgSettings(1e-10, ref["iterations"] - 3))
 
 
 def test_near_unit_links_cg_eo():
@@ -359,14 +406,19 @@ def test_near_unit_links_cg_eo():
 @pytest.mark.parametrize("n,rep,links,fmt", [
     (2, lb.FUNDAMENTAL, lb.LINKS_HAAR, "su2"),
     (2, lb.ADJOINT, lb.LINKS_HAAR, "su2"),
+    (3, lb.FUNDAMENTAL, lb.LINKS_HAAR, "r10"),
+    (3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT, "r10"),
     (3, lb.FUNDAMENTAL, lb.LINKS_HAAR, "r12"),
     (3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT, "r12"),
     (4, lb.ANTISYMMETRIC, lb.LINKS_HAAR, "as4r"),
-], ids=["su2f", "su2a", "su3f", "su3f-near-unit", "su4as"])
+], ids=["su2f", "su2a", "su3f-r10", "su3f-near-unit-r10", "su3f-r12", "su3f-near-unit-r12", "su4as"])
 @pytest.mark.parametrize("bc", [lb.PERIODIC, lb.ANTIPERIODIC_T], ids=["periodic", "antiperiodic"])
-def test_compact_link_storage_is_exact(n, rep, links, fmt, bc):
+def test_compact_link_storage_is_exact(n, rep, links, fmt, bc, monkeypatch):
     """Compact link formats (links.cuh) give the same Dphi as dense storage and
-    the oracle, and download the uploaded links."""
+    the oracle, and download the uploaded links (SU(3): R10 by default, R12
+    with LBCU_SU3_STORAGE=r12)."""
+    if fmt == "r12":
+        monkeypatch.setenv("LBCU_SU3_STORAGE", "r12")
     L = [4, 4, 6, 4]
     dr, g, s = fields(L, n, rep, links=links)
     ctx = lb.Context(L)
@@ -384,6 +436,31 @@ def test_compact_link_storage_is_exact(n, rep, links, fmt, bc):
     assert rel_l2(of.download(), want) < TOL_DPHI
     assert np.abs(gc.download() - g).max() < 1e-12
     assert np.array_equal(gf.download(), g)
+
+
+def test_r10_falls_back_to_r12_when_the_pivot_is_tiny():
+    """R10 divides by U_00: a link with U_00 ~ 1e-14 cannot be rebuilt to
+    1e-12 from 5 entries, so the upload keeps R12 for that field (exact)."""
+    L = [4, 4, 4, 4]
+    g = lb.init_gauge_random(L, 3, lb.FUNDAMENTAL, 1)
+    # an SU(3) link with |U_00| = 1e-13: row 0 fixed, row 1 a random unit
+    # vector orthogonal to it, row 2 = conj(row0 x row1)
+    rng = np.random.default_rng(5)
+    r0 = np.array([1e-13, 0.6 + 0.2j, 0.0])
+    r0[2] = np.sqrt(1 - np.vdot(r0, r0).real)
+    v = rng.normal(size=3) + 1j * rng.normal(size=3)
+    r1 = v - np.vdot(r0, v) * r0
+    r1 /= np.linalg.norm(r1)
+    q = np.array([r0, r1, np.conj(np.cross(r0, r1))])
+    assert np.abs(q @ q.conj().T - np.eye(3)).max() < 1e-14 and abs(np.linalg.det(q) - 1) < 1e-14
+    g[5, 1] = q
+    ctx = lb.Context(L)
+    gauge = lb.GaugeField(ctx, 3, lb.FUNDAMENTAL, lb.ANTIPERIODIC_T).upload(g)
+    assert gauge.storage()[0] == "r12"
+    s = lb.init_spinor_random(L, 3, 1, 0)
+    inp, out = lb.SpinorField(ctx, 3).upload(s), lb.SpinorField(ctx, 3)
+    lb.apply_dirac(out, gauge, inp, 0.1)
+    assert rel_l2(out.download(), O.port_dirac(L, 1, 0.1, g, s)) < TOL_DPHI
 
 
 def test_non_group_links_stay_dense():

@@ -288,3 +288,81 @@ def test_ipc_world_bootstrap_on_host():
         lb.World.ipc(2, 0, "no-leading-slash")
     with pytest.raises(lb.ConfigError):
         lb.World.ipc(9, 0, "/lbcu_too_many")
+
+
+def test_handle_ownership_releases_children_first(monkeypatch):
+    """paper_1401_3733_b200._Owned: whatever order the garbage collector
+    finalises a cycle in, a field's handle is freed before its context's and
+    a context's before its world's, each exactly once (a fake library records
+    the destroy calls; no device needed)."""
+    import gc
+    import paper_1401_3733_b200 as lb
+
+    calls = []
+
+    class FakeLib:
+        def __getattr__(self, name):
+            return lambda h: calls.append((name, h))
+
+    monkeypatch.setattr(lb, "_lib", FakeLib())
+
+    class W(lb._Owned):
+        _destroy = "world_destroy"
+
+    class Cx(lb._Owned):
+        _destroy = "ctx_destroy"
+
+    class F(lb._Owned):
+        _destroy = "field_destroy"
+
+    def make(tag):
+        w = W()
+        w._own(f"w{tag}")
+        c = Cx()
+        c._own(f"c{tag}", w)
+        fs = [F() for _ in range(3)]
+        for k, f in enumerate(fs):
+            f._own(f"f{tag}{k}", c)
+        return w, c, fs
+
+    # explicit close of a middle node
+    w, c, fs = make("a")
+    fs[0].close()
+    c.close()
+    assert calls[0] == ("field_destroy", "fa0") and calls[-1] == ("ctx_destroy", "ca")
+    assert sorted(h for _, h in calls) == ["ca", "fa0", "fa1", "fa2"]
+    fs[1].close()
+    w.close()
+    assert calls[-1] == ("world_destroy", "wa") and len(calls) == 5
+    # a garbage cycle through all three levels
+    calls.clear()
+    w, c, fs = make("b")
+    w.cycle, c.cycle = (c, fs), (w, fs)
+    for f in fs:
+        f.cycle = (w, c)
+    del w, c, fs, f
+    gc.collect()
+    order = [h for _, h in calls]
+    assert sorted(order) == ["cb", "fb0", "fb1", "fb2", "wb"]
+    assert order.index("cb") > max(order.index(f"fb{k}") for k in range(3))
+    assert order.index("wb") == len(order) - 1
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liblatbench_ref.so")),
+                    reason="reference not built")
+def test_reference_arm_reports_the_gpu_arms_workload():
+    """bench.py --impl reference: the unmodified reference on the host on the
+    GPU arm's exact workload description (config dict identical, so the
+    driver can pair the arms), with its own cpu_baseline and a zero-copy e2e."""
+    import json
+    import subprocess
+    import sys
+    import bench
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                        "--steps", "3", "--warmup", "3"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["config"] == json.loads(json.dumps(bench.config_dict(bench.CONFIGS[1], 1)))
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
