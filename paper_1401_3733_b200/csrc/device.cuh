@@ -102,14 +102,19 @@ __device__ __forceinline__ double2 phm(double2 z) {
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
 // a or -a by a sign mask (0 or 1 << 63 in the high word): the +-1 factors of
-// the hop (gamma5 on the input, the antiperiodic time sign) as integer XORs
-// of the sign bits instead of fp64 multiplies (the fp64 pipe is the busiest
-// one in the hop kernel and the power cap binds on the large lattices)
+// the hop (gamma5 on the input, the antiperiodic time sign). As an fp64
+// multiply by default; -DLBCU_SIGN_XOR=1 flips the sign bit with an integer
+// XOR instead (moves the work off the fp64 pipe, but measured 2-4 % slower for
+// the SU(2) hop and neutral for SU(3): profiles/r2e_ab_sign.log)
 __host__ __device__ __forceinline__ unsigned sign_mask(bool neg) { return neg ? 0x80000000u : 0u; }
+#if LBCU_SIGN_XOR
 __device__ __forceinline__ double flip(double a, unsigned m) {
   return __hiloint2double(__double2hiint(a) ^ static_cast<int>(m), __double2loint(a));
 }
 __device__ __forceinline__ double2 cflip(unsigned m, double2 a) { return make_double2(flip(a.x, m), flip(a.y, m)); }
+#else
+__device__ __forceinline__ double2 cflip(unsigned m, double2 a) { return cscale(m ? -1.0 : 1.0, a); }
+#endif
 
 // acc += u * v
 __device__ __forceinline__ void cmac(double2& acc, double2 u, double2 v) {
