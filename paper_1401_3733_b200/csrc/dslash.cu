@@ -316,7 +316,7 @@ __device__ __forceinline__ void hop_z_shared(double2 (&acc)[4][D], const HopArgs
 
 template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS>
 __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1], unsigned mask);
-template <int D, int EPI, int SP0 = 0, int NSP = 4>
+template <int D, int EPI>
 __device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const double2 (&acc)[4][D],
                                          double (&nrm)[1]);
 
@@ -386,108 +386,6 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
 
     epilogue<D, EPI>(A, par, i, acc, nrm);
   }
-}
-
-// ---- experiment: warp-pair direction split (LBCU_HOP_WPS=1, no halos) -----
-// A pair of warps shares 32 output sites: warp 0 of the pair runs the t and x
-// hops, warp 1 the y and z hops, so each thread holds half the loads of a
-// site and the pair issues all 8 hops of its sites at once. The partial
-// accumulators meet in shared memory (each warp hands over the two spin
-// components the other finishes) and each warp runs the epilogue of two spin
-// components. Warp-uniform roles: no divergence.
-constexpr int kWpsSites = 64;  // sites per 128-thread block
-
-__device__ __forceinline__ int sched_site_n(const HopArgs& A, int blk, bool& ok, int tsite, int bsites) {
-  const int Lt = A.g.L[0], Lx = A.g.L[1];
-  const int per_sb = Lt * A.sched_cpb;
-  const int sb = blk / per_sb, rem = blk - sb * per_sb;
-  const int t = rem / A.sched_cpb, chunk = rem - t * A.sched_cpb;
-  const int off = chunk * bsites + tsite;
-  ok = off < A.sched_len;
-  const int row_sites = A.g.vh / (Lt * Lx);
-  return (t * Lx + sb * A.sched_bx) * row_sites + off;
-}
-
-template <int D, bool REAL, int FMT, int EPI, int MINB>
-__global__ void __launch_bounds__(128, MINB) hop_wps_kernel(const __grid_constant__ HopArgs A) {
-  __shared__ double2 xch[2][2][2 * D][32];  // [pair][writer role][2 spins x D][lane]
-  int par, blk;
-  if (A.both) {
-    par = blockIdx.x & 1;
-    blk = blockIdx.x >> 1;
-  } else {
-    par = A.par0;
-    blk = blockIdx.x;
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = warp >> 1, role = warp & 1;
-  const int tsite = pair * 32 + lane;
-  int idx;
-  bool ok;
-  if (A.sched_len > 0) {
-    idx = sched_site_n(A, blk, ok, tsite, kWpsSites);
-  } else {
-    idx = blk * kWpsSites + tsite;
-    ok = idx < A.nsites;
-  }
-  double nrm[1] = {0.0};
-  double2 acc[4][D];
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int cc = 0; cc < D; ++cc) acc[k][cc] = make_double2(0.0, 0.0);
-  int i = 0;
-  if (ok) {
-    i = A.list[par] ? A.list[par][idx] : idx + A.ioff[par];
-    int c[4], s;
-    cb_coords(A.g, i, par, c, s);
-    const double2* in = A.in[par ^ 1];
-    if (role == 0) {
-      hop_mu<D, REAL, FMT, false, 0>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, false, 1>(acc, A, in, par, i, s, c);
-    } else {
-      hop_mu<D, REAL, FMT, false, 2>(acc, A, in, par, i, s, c);
-      hop_mu<D, REAL, FMT, false, 3>(acc, A, in, par, i, s, c);
-    }
-  }
-  // role 0 finishes spins 0, 1 and hands over 2, 3; role 1 the other way round
-  if (role == 0) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) xch[pair][0][k * D + cc][lane] = acc[2 + k][cc];
-  } else {
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) xch[pair][1][k * D + cc][lane] = acc[k][cc];
-  }
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-  if (role == 0) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) acc[k][cc] = cadd(acc[k][cc], xch[pair][1][k * D + cc][lane]);
-    if (ok) {
-      if constexpr (FMT == GF_AS4R) {
-        as4r_out(acc[0], 0.5);
-        as4r_out(acc[1], 0.5);
-      }
-      epilogue<D, EPI, 0, 2>(A, par, i, acc, nrm);
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) acc[2 + k][cc] = cadd(acc[2 + k][cc], xch[pair][0][k * D + cc][lane]);
-    if (ok) {
-      if constexpr (FMT == GF_AS4R) {
-        as4r_out(acc[2], 0.5);
-        as4r_out(acc[3], 0.5);
-      }
-      epilogue<D, EPI, 2, 2>(A, par, i, acc, nrm);
-    }
-  }
-  if constexpr (EPI != EPI_STORE) block_reduce_partial<1>(A.red, nrm);
 }
 
 // ---- experiment: TMA-staged row blocks (full Dphi, SU(2) links, Lz = 32) ----
@@ -643,7 +541,7 @@ __global__ void __launch_bounds__(256, MINB) hop_rowblock_kernel(const __grid_co
 // CG residual update. Two phases: every load (x, r) is issued before any
 // store, and the pointers are restrict-qualified, so the 4 dr round trips
 // overlap instead of serialising behind possible aliasing.
-template <int D, int EPI, int SP0, int NSP>
+template <int D, int EPI>
 __device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const double2 (&acc)[4][D],
                                          double (&nrm)[1]) {
   const long long st = estride(A.g.stride);
@@ -652,7 +550,7 @@ __device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const
   double2* __restrict__ r = A.r[par] ? site_ptr<4 * D>(A.r[par], i) : nullptr;
   double2 xv[4][D], rv[4][D];
 #pragma unroll
-  for (int sp = SP0; sp < SP0 + NSP; ++sp)
+  for (int sp = 0; sp < 4; ++sp)
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) {
       const long long o = (long long)(sp * D + cc) * st;
@@ -661,7 +559,7 @@ __device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const
     }
   const double alpha = (EPI == EPI_CG) ? *A.alpha : 0.0;
 #pragma unroll
-  for (int sp = SP0; sp < SP0 + NSP; ++sp)
+  for (int sp = 0; sp < 4; ++sp)
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) {
       const long long o = (long long)(sp * D + cc) * st;
@@ -986,39 +884,6 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       }
       hop_rowblock_kernel<2, false, GF_SU2, 2><<<nb, 256, smem, s>>>(A);
       ctx->launches += 1;
-      LBCU_CUDA(cudaGetLastError());
-      return;
-    }
-    // experiment: warp-pair direction split (R10 / R12 / SU(2) adjoint links)
-    if (env_int("LBCU_HOP_WPS", 0) && dr == 3 && (fmt == GF_R10 || fmt == GF_R12 || (real && fmt == GF_SU2))) {
-      int wblocks = (A.nsites + kWpsSites - 1) / kWpsSites * npar;
-      if (A.sched_len > 0) {
-        A.sched_cpb = (A.sched_len + kWpsSites - 1) / kWpsSites;
-        wblocks = (geo.local[1] / A.sched_bx) * geo.local[0] * A.sched_cpb * npar;
-      }
-      if (reduce) {
-        if (wblocks > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
-        A.red.total_blocks = wblocks;
-      }
-      const int minb = env_int("LBCU_HOP_WPS_MINB", 4);
-      auto go = [&](auto Fc, auto Rc) {
-        constexpr int F = decltype(Fc)::value;
-        constexpr bool R = decltype(Rc)::value;
-#define LBCU_WPS(E, M) \
-  if (c.epi == E && minb == M) hop_wps_kernel<3, R, F, E, M><<<wblocks, 128, 0, s>>>(A);
-        LBCU_WPS(EPI_STORE, 3) LBCU_WPS(EPI_STORE_NORM, 3) LBCU_WPS(EPI_CG, 3)
-        LBCU_WPS(EPI_STORE, 4) LBCU_WPS(EPI_STORE_NORM, 4) LBCU_WPS(EPI_CG, 4)
-        LBCU_WPS(EPI_STORE, 5) LBCU_WPS(EPI_STORE_NORM, 5) LBCU_WPS(EPI_CG, 5)
-#undef LBCU_WPS
-      };
-      if (fmt == GF_R10) go(std::integral_constant<int, GF_R10>{}, std::false_type{});
-      else if (fmt == GF_R12) go(std::integral_constant<int, GF_R12>{}, std::false_type{});
-      else go(std::integral_constant<int, GF_SU2>{}, std::true_type{});
-      ctx->launches += 1;
-      if (reduce) {
-        k_reduce_finish<1><<<1, kFinishThreads, 0, s>>>(A.red);
-        ctx->launches += 1;
-      }
       LBCU_CUDA(cudaGetLastError());
       return;
     }

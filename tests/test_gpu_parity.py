@@ -601,29 +601,3 @@ def test_dphi_host_pipeline_distinct_fields():
     lb.dphi_host(gauge, m, [x.ctypes.data for x in ins], [y.ctypes.data for y in outs])
     for x, y in zip(ins, outs):
         assert rel_l2(y, O.port_dirac(L, 1, m, g, x)) < TOL_DPHI
-
-
-@pytest.mark.parametrize("minb", ["3", "4", "5"])
-@pytest.mark.parametrize("n,rep,links", [(3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT), (3, lb.FUNDAMENTAL, lb.LINKS_HAAR),
-                                         (2, lb.ADJOINT, lb.LINKS_HAAR)], ids=["r10", "su3f", "su2a"])
-def test_wps_warp_pair_split_matches_oracle(n, rep, links, minb, monkeypatch):
-    """The warp-pair direction-split hop kernel (LBCU_HOP_WPS=1): Dphi, the eo
-    blocks, Mhat and the eo CG against the oracle, with and without the
-    L2-blocked schedule (a lattice whose time slices exceed the budget)."""
-    monkeypatch.setenv("LBCU_HOP_WPS", "1")
-    monkeypatch.setenv("LBCU_HOP_WPS_MINB", minb)
-    for L, l2mb in (([8, 4, 6, 4], "32"), ([8, 8, 8, 8], "0")):  # 0 MB budget: the blocked schedule
-        monkeypatch.setenv("LBCU_HOP_L2MB", l2mb)
-        dr, g, s = fields(L, n, rep, links=links)
-        ctx = lb.Context(L)
-        gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g)
-        inp, out = lb.SpinorField(ctx, dr).upload(s), lb.SpinorField(ctx, dr)
-        lb.apply_dirac(out, gauge, inp, 0.1)
-        assert rel_l2(out.download(), O.port_dirac(L, 1, 0.1, g, s)) < TOL_DPHI
-        e_in = lb.SpinorField(ctx, dr, lb.EVEN).upload(s)
-        e_out = lb.SpinorField(ctx, dr, lb.EVEN)
-        lb.mhat(e_out, gauge, e_in, 0.1)
-        assert rel_l2(e_out.download(), O.port_mhat(L, 1, 0.1, g, s)) < TOL_DPHI
-        o = lb.cg_solve_eo(gauge, 0.1, e_in, lb.CgSettings(1e-10, 500))
-        ref = O.port_cg(L, 1, 1, 0.1, g, s, 1e-10)
-        assert abs(o.iterations - ref["iterations"]) <= 1 and o.true_rel_residual < 2e-10
