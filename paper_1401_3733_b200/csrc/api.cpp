@@ -365,7 +365,6 @@ int lbcu_ctx_destroy(lbcu_ctx c) {
   cudaFreeHost(c->hcg);
   if (c->dhist) cudaFree(c->dhist);
   if (c->staging) cudaFree(c->staging);
-  if (c->fused_ctr) cudaFree(c->fused_ctr);
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaEventDestroy(c->ev_fork);
   cudaEventDestroy(c->ev_pack);
@@ -664,6 +663,7 @@ void mhat_impl(lbcu_spinor_s* out, const lbcu_gauge_s* g, const lbcu_spinor_s* i
   h1.out_parity = 1;
   h1.b = 1.0;
   h1.s5in = g5sandwich ? -1.0 : 1.0;
+  hop_apply(ctx, h1);
   HopCall h2;
   h2.in = t;
   h2.out = out;
@@ -673,11 +673,6 @@ void mhat_impl(lbcu_spinor_s* out, const lbcu_gauge_s* g, const lbcu_spinor_s* i
   h2.a = A;
   h2.b = -1.0 / (4.0 * A);
   if (g5sandwich) h2.s5acc = -1.0;  // g5 (A g5 x - H t/4A) = A x -/+ ...
-  if (mhat_fused_usable(ctx) && g->dr <= 3) {
-    mhat_fused_apply(ctx, h1, h2);
-    return;
-  }
-  hop_apply(ctx, h1);
   hop_apply(ctx, h2);
 }
 }  // namespace

@@ -93,26 +93,18 @@ __device__ __forceinline__ void reconstruct(double2 (&acc)[4][D], const double2 
 // only locates (parity, mu) blocks
 __device__ __forceinline__ long long estride(long long) { return kTile; }
 
-// Spinor loads: the read-only path, or (COH) L2-coherent loads for data that
-// other CTAs wrote earlier in the same launch (the fused Mhat sweep).
-template <bool COH>
-__device__ __forceinline__ double2 ldsp(const double2* p) {
-  if constexpr (COH) return __ldcg(p);
-  else return ldg(p);
-}
-
 // h_a = psi_a + F_a * s5 * psi_{p_a}: spin projection of the spinor at cb site nb
-template <int D, int P0, int P1, int F0, int F1, bool COH = false>
+template <int D, int P0, int P1, int F0, int F1>
 __device__ __forceinline__ void project(double2 (&h)[2][D], const double2* __restrict__ in,
                                         long long st, int nb, unsigned s5) {
   const double2* __restrict__ q = site_ptr<4 * D>(in, nb);
   const long long es = estride(st);
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    const double2 a0 = ldsp<COH>(q + (long long)(0 * D + c) * es);
-    const double2 a1 = ldsp<COH>(q + (long long)(1 * D + c) * es);
-    const double2 b0 = ldsp<COH>(q + (long long)(P0 * D + c) * es);
-    const double2 b1 = ldsp<COH>(q + (long long)(P1 * D + c) * es);
+    const double2 a0 = ldg(q + (long long)(0 * D + c) * es);
+    const double2 a1 = ldg(q + (long long)(1 * D + c) * es);
+    const double2 b0 = ldg(q + (long long)(P0 * D + c) * es);
+    const double2 b1 = ldg(q + (long long)(P1 * D + c) * es);
     h[0][c] = cadd(a0, phm<F0>(cflip(s5, b0)));
     h[1][c] = cadd(a1, phm<F1>(cflip(s5, b1)));
   }
@@ -164,7 +156,7 @@ __device__ __forceinline__ void bc_sign(double2 (&h)[2][D], bool neg) {
   }
 }
 
-template <int D, bool REAL, int FMT, bool BND, int MU, bool COH = false>
+template <int D, bool REAL, int FMT, bool BND, int MU>
 __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
                                        const double2* __restrict__ in, int par, int i, int s,
                                        const int c[4]) {
@@ -180,7 +172,7 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
 #pragma unroll
         for (int cc = 0; cc < D; ++cc) h[a][cc] = ldg(A.hfwd[par][MU] + (a * D + cc) * hc + j);
     } else {
-      project<D, G::p0, G::p1, G::f0, G::f1, COH>(h, in, st, nb_fwd(A.g, s, c, MU) >> 1, A.s5in);
+      project<D, G::p0, G::p1, G::f0, G::f1>(h, in, st, nb_fwd(A.g, s, c, MU) >> 1, A.s5in);
     }
     if constexpr (MU == 0) bc_sign<D, FMT>(h, A.bc_kernel && A.t_off + c[0] == A.bc_tlast);
     link_hop<D, REAL, FMT, false, G::r0, G::r1, G::q0, G::q1>(
@@ -206,7 +198,7 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
     } else {
       double2 h[2][D];
       const int nb = nb_bwd(A.g, s, c, MU) >> 1;
-      project<D, G::p0, G::p1, G::f0 ^ 1, G::f1 ^ 1, COH>(h, in, st, nb, A.s5in);
+      project<D, G::p0, G::p1, G::f0 ^ 1, G::f1 ^ 1>(h, in, st, nb, A.s5in);
       if constexpr (MU == 0) {
         const int tl = c[0] > 0 ? c[0] - 1 : A.g.L[0] - 1;
         bc_sign<D, FMT>(h, A.bc_kernel && A.t_off + tl == A.bc_tlast);
@@ -394,118 +386,6 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
 
     epilogue<D, EPI>(A, par, i, acc, nrm);
   }
-}
-
-// ---- fused Mhat sweep: both eo hops of Mhat in one persistent kernel --------
-// out_e = a x_e + b H_eo (H_oe in_e) (Mhat = A - H_eo H_oe / 4A, or its g5
-// sandwich), with the odd intermediate t_o = H_oe in_e produced and consumed
-// while it is still in L2. The lattice is cut into units of bx x-planes; the
-// units are swept one after another, each along t as a chain of phases
-//   A(T-1), A(0), A(1), B(0), A(2), B(1), ..., A(T-2), B(T-3), B(T-2), B(T-1)
-// where A(s) computes t_o on slice s for x-planes x0-1 .. x0+bx (the two halo
-// planes recomputed, bit-identical to the neighbour unit's) and B(s) the even
-// outputs of slice s from t_o on slices s-1, s, s+1. Work items (unit, phase,
-// chunk of 128 sites) are claimed from one global ticket in that order, so an
-// item only ever waits for items claimed before it by running CTAs: a B chunk
-// spins until the three A phases it reads have all their chunks counted. The
-// t_o reads go through L2 (ld.global.cg): that data is written in the same
-// launch. Units of bx planes keep the live window (~3 slices of one unit) far
-// below the L2 size, so each link is fetched from HBM about once per Mhat
-// instead of twice, and t_o mostly never reaches HBM.
-struct FusedArgs {
-  HopArgs a, b;      // phase A: out = t (odd); phase B: in = t, out (even)
-  int T, Lx, row_sites, bx, nunits, chunks;  // chunks per phase (A size)
-  unsigned long long* ticket;
-  unsigned* done;    // [nunits][T] A-phase chunk counters
-  long long items;
-};
-
-__device__ __forceinline__ void fused_phase(int T, int k, bool& isA, int& slice) {
-  if (k == 0) { isA = true; slice = T - 1; }
-  else if (k == 1) { isA = true; slice = 0; }
-  else if (k >= 2 * T - 2) { isA = false; slice = k - T; }  // B(T-2), B(T-1)
-  else { const int m = (k - 2) >> 1; isA = ((k - 2) & 1) == 0; slice = isA ? m + 1 : m; }
-}
-
-template <int D, bool REAL, int FMT, int EPI, bool COH>
-__device__ __forceinline__ void fused_site(const HopArgs& A, int par, int i, double (&nrm)[1]) {
-  int c[4], s;
-  cb_coords(A.g, i, par, c, s);
-  double2 acc[4][D];
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int cc = 0; cc < D; ++cc) acc[k][cc] = make_double2(0.0, 0.0);
-  const double2* in = A.in[par ^ 1];
-  constexpr int kPerm = (FMT == GF_SU2 || (D == 2 && !REAL)) ? 3210 : 123;
-  auto dir = [&](auto Mc) { hop_mu<D, REAL, FMT, false, decltype(Mc)::value, COH>(acc, A, in, par, i, s, c); };
-  dir(std::integral_constant<int, kPerm / 1000>{});
-  dir(std::integral_constant<int, kPerm / 100 % 10>{});
-  dir(std::integral_constant<int, kPerm / 10 % 10>{});
-  dir(std::integral_constant<int, kPerm % 10>{});
-  if constexpr (FMT == GF_AS4R) {
-#pragma unroll
-    for (int sp = 0; sp < 4; ++sp) as4r_out(acc[sp], 0.5);
-  }
-  epilogue<D, EPI>(A, par, i, acc, nrm);
-}
-
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int D, bool REAL, int FMT, int EPI, int MINB>
-__global__ void __launch_bounds__(128, MINB) mhat_fused_kernel(const __grid_constant__ FusedArgs F) {
-  __shared__ long long item_sh;
-  double nrm[1] = {0.0};
-  const int T = F.T;
-  const long long per_unit = 2LL * T * F.chunks;
-  for (;;) {
-    if (threadIdx.x == 0) item_sh = static_cast<long long>(atomicAdd(F.ticket, 1ULL));
-    __syncthreads();
-    const long long item = item_sh;
-    __syncthreads();  // item_sh is rewritten by the next claim
-    if (item >= F.items) break;
-    const int unit = static_cast<int>(item / per_unit);
-    const long long rem = item - unit * per_unit;
-    const int k = static_cast<int>(rem / F.chunks), chunk = static_cast<int>(rem - (long long)k * F.chunks);
-    bool isA;
-    int slice;
-    fused_phase(T, k, isA, slice);
-    const int x0 = unit * F.bx;
-    if (isA) {
-      const int off = chunk * 128 + threadIdx.x;  // over bx + 2 planes
-      if (off < (F.bx + 2) * F.row_sites) {
-        const int pl = off / F.row_sites;
-        const int x = (x0 - 1 + pl + F.Lx) % F.Lx;
-        const int i = (slice * F.Lx + x) * F.row_sites + (off - pl * F.row_sites);
-        double unused[1] = {0.0};
-        fused_site<D, REAL, FMT, EPI_STORE, false>(F.a, 1, i, unused);
-      }
-      __threadfence();  // every thread's t_o stores before the count
-      __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(F.done + unit * T + slice, 1u);
-    } else {
-      if (threadIdx.x == 0) {  // the three A phases this B phase reads
-        const unsigned need = static_cast<unsigned>(F.chunks);
-        const unsigned* d = F.done + unit * T;
-        const int sm = (slice + T - 1) % T, sp = (slice + 1) % T;
-        while (ld_acquire(d + sm) < need || ld_acquire(d + slice) < need || ld_acquire(d + sp) < need)
-          __nanosleep(64);
-        __threadfence();
-      }
-      __syncthreads();
-      const int off = chunk * 128 + threadIdx.x;  // over bx planes
-      if (off < F.bx * F.row_sites) {
-        const int pl = off / F.row_sites;
-        const int i = (slice * F.Lx + x0 + pl) * F.row_sites + (off - pl * F.row_sites);
-        fused_site<D, REAL, FMT, EPI, true>(F.b, 0, i, nrm);
-      }
-    }
-  }
-  if constexpr (EPI != EPI_STORE) block_reduce_partial<1>(F.b.red, nrm);
 }
 
 // ---- experiment: TMA-staged row blocks (full Dphi, SU(2) links, Lz = 32) ----
@@ -928,10 +808,19 @@ HaloBufs& halo_bufs(lbcu_ctx_s* ctx, int dr) {
 
 }  // namespace
 
-namespace {
-
-HopArgs base_args(lbcu_ctx_s* ctx, const HopCall& c) {
+void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
   const Geometry& geo = ctx->geo;
+  const int dr = c.in->dr;
+  const bool real = c.g->real;
+  const int fmt = c.g->fmt;
+  const int pars[2] = {c.out_parity == 2 ? 0 : c.out_parity, c.out_parity == 2 ? 1 : c.out_parity};
+  const int npar = c.out_parity == 2 ? 2 : 1;
+  for (int k = 0; k < npar; ++k) {
+    const int p = pars[k];
+    if (!c.out->has(p) || !c.in->has(p ^ 1) || (c.x && !c.x->has(p)) || (c.r && !c.r->has(p)))
+      throw Error(LBCU_CONTRACT_VIOLATION, "hop: field subsets do not cover the requested parity");
+  }
+
   HopArgs A{};
   A.g = ctx->dgeo;
   for (int p = 0; p < 2; ++p) {
@@ -947,148 +836,9 @@ HopArgs base_args(lbcu_ctx_s* ctx, const HopCall& c) {
   A.s5x = c.s5x;
   A.s5acc = c.s5acc;
   A.alpha = c.alpha;
-  A.bc_kernel = (c.g->bc == LBCU_BC_ANTIPERIODIC_T && c.g->fmt != GF_FULL) ? 1 : 0;
+  A.bc_kernel = (c.g->bc == LBCU_BC_ANTIPERIODIC_T && fmt != GF_FULL) ? 1 : 0;
   A.t_off = geo.coords[0] * geo.local[0];
   A.bc_tlast = geo.global[0] - 1;
-  return A;
-}
-
-}  // namespace
-
-bool mhat_fused_usable(const lbcu_ctx_s* ctx) {
-  const Geometry& geo = ctx->geo;
-  const char* e = std::getenv("LBCU_CG_FUSED_MHAT");
-  if (!(e && e[0] == '1')) return false;
-  return !geo.any_decomposed && geo.local[0] >= 3 && geo.local[1] >= 2;
-}
-
-void mhat_fused_apply(lbcu_ctx_s* ctx, const HopCall& ca, const HopCall& cb);
-
-// Allocate the sweep counters and resolve the launch sizes for the fields of
-// a CG solve before its graph is captured (cudaMalloc is not capturable):
-// one untimed fused Mhat on scratch even fields.
-void mhat_fused_prepare(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, lbcu_spinor_s* in_e, lbcu_spinor_s* t_o,
-                        lbcu_spinor_s* out_e) {
-  HopCall a;
-  a.in = in_e;
-  a.out = t_o;
-  a.g = g;
-  a.out_parity = 1;
-  HopCall b;
-  b.in = t_o;
-  b.out = out_e;
-  b.x = in_e;
-  b.g = g;
-  b.out_parity = 0;
-  b.a = 1.0;
-  b.b = 1.0;
-  for (int e : {EPI_STORE, EPI_STORE_NORM, EPI_CG}) {  // every epilogue the CG uses, sized once
-    b.epi = e;
-    b.result = ctx->dscal + 20;
-    b.r = e == EPI_CG ? out_e : nullptr;
-    b.alpha = &ctx->dcg->alpha;
-    mhat_fused_apply(ctx, a, b);
-  }
-}
-
-// out_e = a x + b H_eo H_oe in_e in one launch (see mhat_fused_kernel):
-// ca: the H_oe call (in even -> t odd, EPI_STORE), cb: the H_eo call
-// (in = t, out / x / r even, any epilogue). Both share the gauge field.
-void mhat_fused_apply(lbcu_ctx_s* ctx, const HopCall& ca, const HopCall& cb) {
-  const Geometry& geo = ctx->geo;
-  if (ca.out_parity != 1 || cb.out_parity != 0 || ca.epi != EPI_STORE || ca.out != cb.in || ca.g != cb.g)
-    throw Error(LBCU_CONTRACT_VIOLATION, "fused Mhat: expects H_oe then H_eo on its output");
-  const int dr = ca.in->dr;
-  const bool real = ca.g->real;
-  const int fmt = ca.g->fmt;
-  FusedArgs F{};
-  F.a = base_args(ctx, ca);
-  F.b = base_args(ctx, cb);
-  F.a.nsites = F.b.nsites = static_cast<int>(geo.vh);
-  F.T = geo.local[0];
-  F.Lx = geo.local[1];
-  F.row_sites = geo.local[2] * geo.local[3] / 2;
-  // unit width: the largest divisor of Lx whose (bx + 2)-plane slice of both
-  // parities (spinor in + t + out, links as stored) stays under the budget
-  const int lb = fmt == GF_SU2 ? 32 : fmt == GF_R12 ? 96 : fmt == GF_R10 ? 80 : fmt == GF_AS4 ? 256
-                 : fmt == GF_AS4R ? 288 : dr * dr * (real ? 8 : 16);
-  const double plane = 2.0 * F.row_sites * (3 * 64.0 * dr + 4 * lb);
-  const double budget = env_int("LBCU_FUSED_L2MB", 24) * 1e6;
-  F.bx = 1;
-  for (int d = 1; d <= F.Lx; ++d)
-    if (F.Lx % d == 0 && (d + 2) * plane <= budget) F.bx = d;
-  F.nunits = F.Lx / F.bx;
-  F.chunks = ((F.bx + 2) * F.row_sites + 127) / 128;
-  F.items = static_cast<long long>(F.nunits) * 2 * F.T * F.chunks;
-  // counters: [ticket][nunits * T], zeroed per launch (stream-ordered, capturable);
-  // allocated ahead of any graph capture by mhat_fused_prepare
-  const size_t cbytes = sizeof(unsigned long long) + sizeof(unsigned) * F.nunits * F.T;
-  if (ctx->fused_bytes < cbytes) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    LBCU_CUDA(cudaStreamIsCapturing(ctx->stream, &cs));
-    if (cs != cudaStreamCaptureStatusNone)
-      throw Error(LBCU_CUDA_ERROR, "fused Mhat: counters not allocated before graph capture");
-    if (ctx->fused_ctr) LBCU_CUDA(cudaFree(ctx->fused_ctr));
-    ctx->fused_ctr = nullptr;
-    LBCU_CUDA(cudaMalloc(&ctx->fused_ctr, cbytes));
-    ctx->fused_bytes = cbytes;
-  }
-  F.ticket = static_cast<unsigned long long*>(ctx->fused_ctr);
-  F.done = reinterpret_cast<unsigned*>(F.ticket + 1);
-  cudaStream_t s = ctx->stream;
-  LBCU_CUDA(cudaMemsetAsync(ctx->fused_ctr, 0, cbytes, s));
-  const bool reduce = cb.epi != EPI_STORE;
-  dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-    constexpr int D = decltype(Dc)::value;
-    constexpr bool R = decltype(Rc)::value;
-    constexpr int FM = decltype(Fc)::value;
-    if constexpr (D <= 3) {
-      constexpr int MINB = (FM == GF_SU2 && !R) ? 4 : 3;
-      auto launch = [&](auto kern) {
-        static int grid = 0;  // per instantiation: one resident wave of CTAs
-        if (grid == 0) {
-          int per_sm = 0, dev = 0, sms = 0;
-          LBCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
-          LBCU_CUDA(cudaGetDevice(&dev));
-          LBCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-          grid = sms * std::max(per_sm, 1);
-        }
-        if (reduce) {
-          if (grid > ctx->max_partials) throw Error(LBCU_CUDA_ERROR, "reduction workspace too small");
-          F.b.red = Reduce{ctx->partials, cb.result, 0, grid, cb.post, ctx->dcg, ctx->dhist, cb.handle,
-                           cb.use_graph};
-        }
-        kern<<<grid, 128, 0, s>>>(F);
-        ctx->launches += 1;
-        if (reduce) {
-          k_reduce_finish<1><<<1, kFinishThreads, 0, s>>>(F.b.red);
-          ctx->launches += 1;
-        }
-      };
-      if (cb.epi == EPI_STORE) launch(mhat_fused_kernel<D, R, FM, EPI_STORE, MINB>);
-      else if (cb.epi == EPI_STORE_NORM) launch(mhat_fused_kernel<D, R, FM, EPI_STORE_NORM, MINB>);
-      else launch(mhat_fused_kernel<D, R, FM, EPI_CG, MINB>);
-    } else {
-      throw Error(LBCU_CONTRACT_VIOLATION, "fused Mhat: representation dimension > 3");
-    }
-  });
-  LBCU_CUDA(cudaGetLastError());
-}
-
-void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
-  const Geometry& geo = ctx->geo;
-  const int dr = c.in->dr;
-  const bool real = c.g->real;
-  const int fmt = c.g->fmt;
-  const int pars[2] = {c.out_parity == 2 ? 0 : c.out_parity, c.out_parity == 2 ? 1 : c.out_parity};
-  const int npar = c.out_parity == 2 ? 2 : 1;
-  for (int k = 0; k < npar; ++k) {
-    const int p = pars[k];
-    if (!c.out->has(p) || !c.in->has(p ^ 1) || (c.x && !c.x->has(p)) || (c.r && !c.r->has(p)))
-      throw Error(LBCU_CONTRACT_VIOLATION, "hop: field subsets do not cover the requested parity");
-  }
-
-  HopArgs A = base_args(ctx, c);
   const bool reduce = c.epi != EPI_STORE;
   cudaStream_t s = ctx->stream;
 

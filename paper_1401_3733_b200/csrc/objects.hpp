@@ -82,8 +82,6 @@ struct lbcu_ctx_s {
   size_t staging_bytes = 0;
   long long launches = 0;
   long long xepoch = 0;  // halo exchanges so far (direct transports: arena / event slot)
-  void* fused_ctr = nullptr;  // fused Mhat sweep: ticket + per-(unit, slice) counters
-  size_t fused_bytes = 0;
   cudaEvent_t ev_cg[2] = {nullptr, nullptr};  // per-iteration CG state copies (host loop)
   // host-field pipeline (lbcu_dphi_host): 2 slots, copy-in / copy-out streams
   struct HostPipe {
@@ -116,12 +114,6 @@ struct HopCall {
   int use_graph = 0;
 };
 void hop_apply(lbcu_ctx_s* ctx, const HopCall& c);
-// Mhat-shaped pair H_oe then H_eo as one persistent sweep (dslash.cu);
-// usable on single-rank contexts when LBCU_CG_FUSED_MHAT=1
-bool mhat_fused_usable(const lbcu_ctx_s* ctx);
-void mhat_fused_apply(lbcu_ctx_s* ctx, const HopCall& ca, const HopCall& cb);
-void mhat_fused_prepare(lbcu_ctx_s* ctx, const lbcu_gauge_s* g, lbcu_spinor_s* in_e, lbcu_spinor_s* t_o,
-                        lbcu_spinor_s* out_e);
 
 // flat BLAS over the present parity blocks (padding included, kept at zero)
 void blas_sqnorm(lbcu_ctx_s* ctx, const lbcu_spinor_s* f, double* dres);

@@ -83,14 +83,12 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
   };
   cg_p_update(ctx, p, r, x);
   if (F.kind == Fused::EO) {
-    // both hops of each Mhat as one sweep kernel when enabled (dslash.cu)
-    const bool fm = mhat_fused_usable(ctx) && F.g->dr <= 3;
     HopCall a;  // t_o = H_oe p_e
     a.in = p;
     a.out = t;
     a.g = F.g;
     a.out_parity = 1;
-    if (!fm) hop_apply(ctx, a);
+    hop_apply(ctx, a);
     HopCall b;  // q_e = Mhat p_e = A p - H_eo t / 4A ; |q|^2
     b.in = t;
     b.out = q;
@@ -102,8 +100,7 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
     b.epi = EPI_STORE_NORM;
     b.result = slot(ctx, kSlotPap);
     scalar_alpha(b);
-    if (fm) mhat_fused_apply(ctx, a, b);
-    else hop_apply(ctx, b);
+    hop_apply(ctx, b);
     after_pap();
     HopCall c;  // t_o = H_oe g5 q
     c.in = q;
@@ -111,7 +108,7 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
     c.g = F.g;
     c.out_parity = 1;
     c.s5in = -1.0;
-    if (!fm) hop_apply(ctx, c);
+    hop_apply(ctx, c);
     HopCall d;  // Ap = g5 Mhat g5 q ; r -= alpha Ap ; |r|^2
     d.in = t;
     d.out = q;  // unused by EPI_CG
@@ -126,8 +123,7 @@ void fused_body(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spinor_s
     d.alpha = &ctx->dcg->alpha;
     d.result = slot(ctx, kSlotRR);
     scalar_end(d);
-    if (fm) mhat_fused_apply(ctx, c, d);
-    else hop_apply(ctx, d);
+    hop_apply(ctx, d);
   } else {
     HopCall a;  // q = D p ; |q|^2 = <p, D^dag D p>
     a.in = p;
@@ -278,7 +274,7 @@ void callback_body(lbcu_ctx_s* ctx, lbcu_linop op, void* user, lbcu_spinor_s* x,
 // can never see freed memory or a stale kernel specialisation, even when a
 // new handle is allocated at a recycled address.
 struct GraphKey {
-  int kind, fmt, fused_mhat;  // fused_mhat: the kernel variant captured (LBCU_CG_FUSED_MHAT)
+  int kind, fmt;
   const void *g, *x, *r, *p, *q, *t;              // handles
   const void *gb, *xb, *rb, *pb, *qb, *tb;        // device bases
   double mass;
@@ -306,7 +302,6 @@ GraphEntry graph_for(lbcu_ctx_s* ctx, const Fused& F, lbcu_spinor_s* x, lbcu_spi
   std::memset(&key, 0, sizeof(key));
   key.kind = F.kind;
   key.fmt = F.g->fmt;
-  key.fused_mhat = F.kind == Fused::EO && mhat_fused_usable(ctx) && F.g->dr <= 3;
   key.g = F.g;
   key.x = x;
   key.r = r;
@@ -404,9 +399,6 @@ int run_cg(lbcu_ctx_s* ctx, const lbcu_cg_settings* st, lbcu_spinor_s* rhs, lbcu
   if (use_graph) {  // capture + instantiate (first solve on these fields) outside the timed region
     if (fused->kind == Fused::EO) {  // make sure lazily allocated buffers exist before capture
       (void)scratch_spinor(ctx, dr, LBCU_ODD, 200 + kSlotT);
-      if (mhat_fused_usable(ctx) && dr <= 3)
-        mhat_fused_prepare(ctx, fused->g, scratch_spinor(ctx, dr, sub, 200 + kSlotAp), t,
-                           scratch_spinor(ctx, dr, sub, 200 + kSlotTmp2));
     }
     ge = graph_for(ctx, *fused, x, r, p, q, t);
   }

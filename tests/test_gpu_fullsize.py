@@ -129,16 +129,3 @@ def test_full_size_plain_cg(c):
     assert abs(o.iterations - int(z["h_iterations"])) <= 1, (o.iterations, int(z["h_iterations"]))
     k = min(10, o.iterations, len(z["h_history"]))
     assert np.allclose(o.residual_history[:k], z["h_history"][:k], rtol=1e-6)
-
-
-@pytest.mark.parametrize("c", [2, 3])
-def test_full_size_eo_cg_fused_mhat(c, monkeypatch):
-    """The eo CG with the fused Mhat sweep at full size: the reference's
-    iteration count +-1 and the tolerance met."""
-    monkeypatch.setenv("LBCU_CG_FUSED_MHAT", "1")
-    cfg, ctx, gauge, dr = setup_cfg(c)
-    rhs = lb.SpinorField(ctx, dr, lb.EVEN).randomize(1, 0)
-    o = lb.cg_solve_eo(gauge, cfg["mass"], rhs, lb.CgSettings(cfg["tol"], 5000))
-    z = golden_cg(c)
-    assert o.true_rel_residual < 2 * cfg["tol"]
-    assert abs(o.iterations - int(z["eo_iterations"])) <= 1

@@ -601,36 +601,3 @@ def test_dphi_host_pipeline_distinct_fields():
     lb.dphi_host(gauge, m, [x.ctypes.data for x in ins], [y.ctypes.data for y in outs])
     for x, y in zip(ins, outs):
         assert rel_l2(y, O.port_dirac(L, 1, m, g, x)) < TOL_DPHI
-
-
-@pytest.mark.parametrize("l2mb", ["0", "24"], ids=["units-of-1-plane", "default-units"])
-@pytest.mark.parametrize("n,rep,links", [(3, lb.FUNDAMENTAL, lb.LINKS_NEAR_UNIT), (3, lb.FUNDAMENTAL, lb.LINKS_HAAR),
-                                         (2, lb.FUNDAMENTAL, lb.LINKS_HAAR), (2, lb.ADJOINT, lb.LINKS_HAAR)],
-                         ids=["r10", "su3f", "su2f", "su2a"])
-def test_fused_mhat_sweep_matches_oracle(n, rep, links, l2mb, monkeypatch):
-    """The fused Mhat sweep (LBCU_CG_FUSED_MHAT=1: both eo hops in one
-    persistent kernel, t_o consumed through L2 across CTAs): Mhat, Mhat^dag
-    Mhat and the eo CG against the oracle, with units of one x-plane (most
-    cross-unit halo recomputation) and the default unit width, on lattices
-    with T = 4 (the shortest sweep) and T = 8."""
-    monkeypatch.setenv("LBCU_CG_FUSED_MHAT", "1")
-    monkeypatch.setenv("LBCU_FUSED_L2MB", l2mb)
-    for L in ([4, 6, 4, 8], [8, 4, 6, 4]):
-        dr, g, s = fields(L, n, rep, links=links)
-        ctx = lb.Context(L)
-        gauge = lb.GaugeField(ctx, n, rep, lb.ANTIPERIODIC_T).upload(g)
-        e_in = lb.SpinorField(ctx, dr, lb.EVEN).upload(s)
-        e_out = lb.SpinorField(ctx, dr, lb.EVEN)
-        for _ in range(3):  # repeated launches reuse the counters
-            lb.mhat(e_out, gauge, e_in, 0.1)
-            assert rel_l2(e_out.download(), O.port_mhat(L, 1, 0.1, g, s)) < TOL_DPHI
-        lb.mhat_dag_mhat(e_out, gauge, e_in, 0.1)
-        m1 = O.port_mhat(L, 1, 0.1, g, s)
-        m1[:, 2:] *= -1
-        m2 = O.port_mhat(L, 1, 0.1, g, m1)
-        m2[:, 2:] *= -1
-        assert rel_l2(e_out.download(), m2) < TOL_DPHI
-        o = lb.cg_solve_eo(gauge, 0.1, e_in, lb.CgSettings(1e-10, 500))
-        ref = O.port_cg(L, 1, 1, 0.1, g, s, 1e-10)
-        assert abs(o.iterations - ref["iterations"]) <= 1 and o.true_rel_residual < 2e-10
-        assert rel_l2(o.solution.download(), ref["x"]) < 1e-8
