@@ -17,8 +17,10 @@
 // context on GPU rank % device_count, shared by every call with the same
 // global lattice and worker grid; a multi-worker group becomes an in-process
 // thread world, so the calls stay collective exactly as in the reference.
-// Links are uploaded once per GaugeField (again when its storage moves);
-// after changing link values in place call invalidate(gauge). The BC is
+// Links are uploaded once per GaugeField (again when its storage moves or a
+// 256-value fingerprint of the links changes); after changing link values
+// in place call invalidate(gauge). Worker contexts are keyed by (global
+// lattice, grid, rank): two groups of the same shape must not run at once. The BC is
 // whatever the links carry (an antiperiodic sign baked into U_0 by the caller
 // is reproduced as given). Spinors cross PCIe in the reference's interior
 // layout on every call; halo slots of `in` are not written (the reference
@@ -44,6 +46,8 @@
 #include <latbench/transport.hpp>
 
 #include <array>
+#include <cstdint>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
@@ -76,7 +80,24 @@ struct DeviceGauge {
   lbcu_gauge h = nullptr;
   const void* data = nullptr;  // host storage the upload came from
   size_t size = 0;
+  uint64_t sample = 0;         // fingerprint of 256 strided link values
 };
+
+// Fingerprint of the host links: 256 values spread over the whole array, so
+// a GaugeField re-created at a recycled address (same vector storage, new
+// links) is not mistaken for the uploaded one. In-place edits that miss the
+// sampled entries still need invalidate().
+inline uint64_t link_sample(const double* v, size_t n) {
+  uint64_t h = 0x9e3779b97f4a7c15ULL ^ n;
+  if (n == 0) return h;
+  const size_t step = n / 256 + 1;
+  for (size_t i = 0; i < n; i += step) {
+    uint64_t bits;
+    std::memcpy(&bits, v + i, sizeof(bits));
+    h = (h ^ bits) * 0x100000001b3ULL;
+  }
+  return h;
+}
 
 struct RankState {
   lbcu_ctx ctx = nullptr;
@@ -130,9 +151,10 @@ inline RankState& rank_state(latbench::Worker& w, const latbench::Geometry& geo)
 inline lbcu_gauge device_gauge(RankState& rs, const latbench::GaugeField& g) {
   const void* data = g.real_links ? static_cast<const void*>(g.rdata.data()) : g.cdata.data();
   const size_t size = g.real_links ? g.rdata.size() : g.cdata.size();
+  const uint64_t sample = link_sample(static_cast<const double*>(data), size * (g.real_links ? 1 : 2));
   std::lock_guard<std::mutex> lk(registry().m);  // invalidate() may scan the maps
   DeviceGauge& dg = rs.gauges[&g];
-  if (dg.h && dg.data == data && dg.size == size) return dg.h;
+  if (dg.h && dg.data == data && dg.size == size && dg.sample == sample) return dg.h;
   if (dg.h) lbcu_gauge_destroy(dg.h);
   dg = DeviceGauge{};
   lbcu_gauge h = nullptr;
@@ -146,6 +168,7 @@ inline lbcu_gauge device_gauge(RankState& rs, const latbench::GaugeField& g) {
   dg.h = h;
   dg.data = data;
   dg.size = size;
+  dg.sample = sample;
   return h;
 }
 
