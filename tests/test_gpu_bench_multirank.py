@@ -1,7 +1,8 @@
-"""bench.py's N > 1 flow (torchrun, decomposition, IPC world with direct
+"""bench.py: the N > 1 flow (torchrun, decomposition, IPC world with direct
 halos, decomposed CG, end-to-end host path) run with every rank on the one
 GPU of the test box (--emulate: gloo for the Python-side collectives, host CG
-sums; nothing waits on another rank inside a kernel). Correctness only."""
+sums; nothing waits on another rank inside a kernel; correctness only), the
+one-GPU bench line and a stock-regime line."""
 import json
 import os
 import subprocess
@@ -64,3 +65,17 @@ def test_bench_single_gpu_line():
     assert sorted(line["configs"]) == ["1", "2", "3", "4", "5"]
     assert all(row["cpu_reference_gflops"] > 0 for row in line["configs"].values())
     assert "sm_mhz" in line["clocks"]
+
+
+def test_bench_regime_line():
+    """bench.py --regime: a stock regime at 64x32^3 with the GPU Dphi checked
+    against the unmodified reference apply_dirac on the same host inputs."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--regime", "comms", "--steps", "5", "--warmup", "3",
+           "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["regime"] == "comms" and line["config"]["lattice_TXYZ"] == [64, 32, 32, 32]
+    assert line["parity_vs_reference_rel_l2"] < 1e-12
+    assert line["cg"]["eo"]["iterations"] > 0 and line["cg"]["eo"]["true_rel_residual"] < 2e-10
+    assert line["value"] > 0 and line["roofline"]["frac"] > 0
