@@ -67,12 +67,12 @@ struct HopArgs {
 };
 
 // block index (per parity) + thread -> cb site under the L2-blocked schedule
-__device__ __forceinline__ int sched_site(const HopArgs& A, int blk, bool& ok) {
+__device__ __forceinline__ int sched_site(const HopArgs& A, int blk, int bsz, int tid, bool& ok) {
   const int Lt = A.g.L[0], Lx = A.g.L[1];
   const int per_sb = Lt * A.sched_cpb;
   const int sb = blk / per_sb, rem = blk - sb * per_sb;
   const int t = rem / A.sched_cpb, chunk = rem - t * A.sched_cpb;
-  const int off = chunk * blockDim.x + threadIdx.x;
+  const int off = chunk * bsz + tid;
   ok = off < A.sched_len;
   const int row_sites = A.g.vh / (Lt * Lx);  // cb sites per x-plane of a slice
   return (t * Lx + sb * A.sched_bx) * row_sites + off;
@@ -131,16 +131,103 @@ __device__ __forceinline__ const ElemT<D, REAL, FMT>* link_ptr(const void* gauge
 
 // Multiply by the link and reconstruct into acc. Small dr: row-fused (no
 // intermediate g); large dr: the two-phase form schedules better.
-template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
+template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1, bool SM = false>
 __device__ __forceinline__ void link_hop(double2 (&acc)[4][D], const ElemT<D, REAL, FMT>* p,
                                          long long st, const double2 (&h)[2][D]) {
   if constexpr (D <= 3 || FMT == GF_AS4 || FMT == GF_AS4R) {
-    link_mul_acc<D, REAL, FMT, DAG, R0, R1, Q0, Q1>(acc, p, estride(st), h);
+    link_mul_acc<D, REAL, FMT, DAG, R0, R1, Q0, Q1, SM>(acc, p, estride(st), h);
   } else {
     double2 g[2][D];
-    link_mul<D, REAL, FMT, DAG>(g, p, estride(st), h);
+    link_mul<D, REAL, FMT, DAG, SM>(g, p, estride(st), h);
     reconstruct<D, R0, R1, Q0, Q1>(acc, g);
   }
+}
+
+// ---- warp-private link staging ------------------------------------------------
+// The hop is bound by the bytes its warps keep in flight, and every byte a
+// thread loads with LDG holds a destination register from issue to use. The
+// link tiles a warp needs at its own cb tile (the four forward links) and at
+// the tile shifted by a whole number of tiles (backward t and x links) are
+// contiguous entries x 512 B runs in the tiled layout, so lane 0 fetches them
+// with one bulk async copy each (cp.async.bulk, completion counted on a
+// warp-private mbarrier) into shared memory at the top of the kernel: up to 7
+// link tiles per warp travel without holding a register, and the hops read
+// them back with conflict-free LDS.128 at the same in-tile offsets.
+// Slots: 0-3 forward mu = t, x, y, z (output parity, own tile); 4, 5 backward
+// t, x (input parity, the neighbour's tile); 6 the input-parity z link at the
+// own tile (hop_z_shared). A kernel stages slots [0, NL).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <int D, bool REAL, int FMT, int NL>
+struct LinkStage {
+  using Elem = ElemT<D, REAL, FMT>;
+  static constexpr int TILE = LinkFmt<D, REAL, FMT>::entries * kTile;  // elements per tile
+  static constexpr int slots = NL;
+  const Elem* lane = nullptr;  // this lane's entry 0 of slot 0
+  unsigned bar = 0;
+  bool ready = false;
+  __device__ __forceinline__ void wait() {
+    if constexpr (NL > 0) {
+      if (!ready) {
+        unsigned done = 0;
+        while (!done)
+          asm volatile(
+              "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+              : "=r"(done)
+              : "r"(bar), "r"(0u)
+              : "memory");
+        ready = true;
+      }
+    }
+  }
+  template <int SLOT>
+  __device__ __forceinline__ const Elem* slot() const {
+    return lane + SLOT * TILE;
+  }
+};
+
+template <int D, bool REAL, int FMT, int NL>
+__device__ __forceinline__ LinkStage<D, REAL, FMT, NL> stage_links(const void* gauge, const DevGeo& g, int par,
+                                                                   int i, int s, const int c[4]) {
+  LinkStage<D, REAL, FMT, NL> ls;
+  if constexpr (NL > 0) {
+    using Elem = ElemT<D, REAL, FMT>;
+    constexpr int TILE = LinkStage<D, REAL, FMT, NL>::TILE;
+    constexpr int E = LinkFmt<D, REAL, FMT>::entries;
+    extern __shared__ __align__(128) unsigned char ls_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    Elem* w = reinterpret_cast<Elem*>(ls_raw) + (size_t)warp * NL * TILE;
+    unsigned long long* bar =
+        reinterpret_cast<unsigned long long*>(ls_raw + (size_t)nw * NL * TILE * sizeof(Elem)) + warp;
+    ls.lane = w + lane;
+    ls.bar = smem_u32(bar);
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ls.bar), "r"(1));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ls.bar),
+                   "r"((unsigned)(NL * TILE * sizeof(Elem)))
+                   : "memory");
+      const Elem* gb = static_cast<const Elem*>(gauge);
+      auto copy = [&](int slot, int pp, int mu, int site) {
+        const Elem* src = gb + (long long)(pp * 4 + mu) * E * g.stride + (long long)(site >> 5) * TILE;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(w + slot * TILE)),
+            "l"(src), "r"((unsigned)(TILE * sizeof(Elem))), "r"(ls.bar)
+            : "memory");
+      };
+#pragma unroll
+      for (int mu = 0; mu < 4; ++mu)
+        if (mu < NL) copy(mu, par, mu, i);
+      if constexpr (NL > 4) copy(4, par ^ 1, 0, nb_bwd(g, s, c, 0) >> 1);
+      if constexpr (NL > 5) copy(5, par ^ 1, 1, nb_bwd(g, s, c, 1) >> 1);
+      if constexpr (NL > 6) copy(6, par ^ 1, 3, i);
+    }
+    __syncwarp();
+  }
+  return ls;
 }
 
 // Antiperiodic-t sign of a compact link (dense links carry it baked in):
@@ -156,10 +243,10 @@ __device__ __forceinline__ void bc_sign(double2 (&h)[2][D], bool neg) {
   }
 }
 
-template <int D, bool REAL, int FMT, bool BND, int MU>
+template <int D, bool REAL, int FMT, bool BND, int MU, class LS>
 __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
                                        const double2* __restrict__ in, int par, int i, int s,
-                                       const int c[4]) {
+                                       const int c[4], LS& ls) {
   using G = Gam<MU>;
   const long long st = A.g.stride;
   auto fwd = [&] {  // forward: (1 - g_mu) U_mu(x) in(x + mu)
@@ -175,8 +262,13 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
       project<D, G::p0, G::p1, G::f0, G::f1>(h, in, st, nb_fwd(A.g, s, c, MU) >> 1, A.s5in);
     }
     if constexpr (MU == 0) bc_sign<D, FMT>(h, A.bc_kernel && A.t_off + c[0] == A.bc_tlast);
-    link_hop<D, REAL, FMT, false, G::r0, G::r1, G::q0, G::q1>(
-        acc, link_ptr<D, REAL, FMT>(A.gauge, st, par, MU, i), st, h);
+    if constexpr (MU < LS::slots) {
+      ls.wait();
+      link_hop<D, REAL, FMT, false, G::r0, G::r1, G::q0, G::q1, true>(acc, ls.template slot<MU>(), st, h);
+    } else {
+      link_hop<D, REAL, FMT, false, G::r0, G::r1, G::q0, G::q1>(
+          acc, link_ptr<D, REAL, FMT>(A.gauge, st, par, MU, i), st, h);
+    }
   };
   auto bwd = [&] {  // backward: (1 + g_mu) U_mu(x - mu)^dag in(x - mu)
     if (BND && !A.g.wrap[MU] && c[MU] == 0) {
@@ -203,8 +295,14 @@ __device__ __forceinline__ void hop_mu(double2 (&acc)[4][D], const HopArgs& A,
         const int tl = c[0] > 0 ? c[0] - 1 : A.g.L[0] - 1;
         bc_sign<D, FMT>(h, A.bc_kernel && A.t_off + tl == A.bc_tlast);
       }
-      link_hop<D, REAL, FMT, true, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(
-          acc, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, MU, nb), st, h);
+      if constexpr (MU < 2 && 4 + MU < LS::slots) {
+        ls.wait();
+        link_hop<D, REAL, FMT, true, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1, true>(acc, ls.template slot<4 + MU>(),
+                                                                                st, h);
+      } else {
+        link_hop<D, REAL, FMT, true, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(
+            acc, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, MU, nb), st, h);
+      }
     }
   };
 #ifndef LBCU_HOP_BWDFIRST
@@ -252,11 +350,11 @@ __device__ __forceinline__ void to_frame(double2 (&h)[2][D]) {
 }
 
 // g = M h in the accumulator frame, M = U or U^dag
-template <int D, bool REAL, int FMT, bool DAG>
+template <int D, bool REAL, int FMT, bool DAG, bool SM = false>
 __device__ __forceinline__ void mul_frame(double2 (&g)[2][D], const ElemT<D, REAL, FMT>* p,
                                           const double2 (&h)[2][D]) {
-  if constexpr (FMT == GF_AS4R) as4r_mul<DAG>(g, p, kTile, h);
-  else link_mul<D, REAL, FMT, DAG>(g, p, kTile, h);
+  if constexpr (FMT == GF_AS4R) as4r_mul<DAG, SM>(g, p, kTile, h);
+  else link_mul<D, REAL, FMT, DAG, SM>(g, p, kTile, h);
 }
 
 template <int D>
@@ -276,10 +374,10 @@ __device__ __forceinline__ double2 shfl_d2(unsigned mask, double2 v, int src) {
 // the consumer's backward hop) or P- w (dz = 1: the consumer's forward hop,
 // multiplied by the consumer's own U_z^p). Same arithmetic as hop_mu<3>, one
 // spinor load per site fewer.
-template <int D, bool REAL, int FMT>
+template <int D, bool REAL, int FMT, class LS>
 __device__ __forceinline__ void hop_z_shared(double2 (&acc)[4][D], const HopArgs& A,
                                              const double2* __restrict__ in, int par, int i, int s,
-                                             unsigned mask) {
+                                             unsigned mask, LS& ls) {
   using G = Gam<3>;
   const long long st = A.g.stride;
   const int dz = s & 1;
@@ -293,7 +391,12 @@ __device__ __forceinline__ void hop_z_shared(double2 (&acc)[4][D], const HopArgs
   project2<D, G::p0, G::p1, G::f0, G::f1>(hm, hp, in, i, A.s5in);
   to_frame<D, FMT>(hm);
   to_frame<D, FMT>(hp);
-  mul_frame<D, REAL, FMT, true>(gb, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, 3, i), hp);
+  if constexpr (6 < LS::slots) {
+    ls.wait();
+    mul_frame<D, REAL, FMT, true, true>(gb, ls.template slot<6>(), hp);
+  } else {
+    mul_frame<D, REAL, FMT, true>(gb, link_ptr<D, REAL, FMT>(A.gauge, st, par ^ 1, 3, i), hp);
+  }
   double2 r[2][D];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -309,21 +412,31 @@ __device__ __forceinline__ void hop_z_shared(double2 (&acc)[4][D], const HopArgs
       gb[a][c] = b;
     }
   double2 gf[2][D];
-  mul_frame<D, REAL, FMT, false>(gf, link_ptr<D, REAL, FMT>(A.gauge, st, par, 3, i), hm);
+  if constexpr (3 < LS::slots) {
+    ls.wait();
+    mul_frame<D, REAL, FMT, false, true>(gf, ls.template slot<3>(), hm);
+  } else {
+    mul_frame<D, REAL, FMT, false>(gf, link_ptr<D, REAL, FMT>(A.gauge, st, par, 3, i), hm);
+  }
   reconstruct<D, G::r0, G::r1, G::q0, G::q1>(acc, gf);
   reconstruct<D, G::r0, G::r1, G::q0 ^ 1, G::q1 ^ 1>(acc, gb);
 }
 
-template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS>
+template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS, int NL>
 __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1], unsigned mask);
 template <int D, int EPI>
 __device__ __forceinline__ void epilogue(const HopArgs& A, int par, int i, const double2 (&acc)[4][D],
                                          double (&nrm)[1]);
 
-template <int D, bool REAL, int FMT, bool BND, int EPI, int MINB, bool ZS>
+template <int D, bool REAL, int FMT, bool BND, int EPI, int MINB, bool ZS, int NL = 0>
 __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ HopArgs A) {
-  int par, blk;
-  if (A.both) {
+  int par, blk, bsz = blockDim.x, tid = threadIdx.x;
+  if (A.both == 2) {  // both parities of one cb range in a block: warps [0, n/2) parity 0, the rest parity 1
+    bsz = blockDim.x >> 1;
+    par = threadIdx.x >= bsz;
+    tid = threadIdx.x - par * bsz;
+    blk = blockIdx.x;
+  } else if (A.both) {
     par = blockIdx.x & 1;
     blk = blockIdx.x >> 1;
   } else {
@@ -334,26 +447,28 @@ __global__ void __launch_bounds__(128, MINB) hop_kernel(const __grid_constant__ 
   int idx;
   bool ok;
   if (A.sched_len > 0) {
-    idx = sched_site(A, blk, ok);
+    idx = sched_site(A, blk, bsz, tid, ok);
   } else {
-    idx = blk * blockDim.x + threadIdx.x;
+    idx = blk * bsz + tid;
     ok = idx < A.nsites;
   }
   if constexpr (ZS) {
     const unsigned mask = __ballot_sync(0xffffffffu, ok);
-    if (ok) site_body<D, REAL, FMT, BND, EPI, ZS>(A, par, idx, nrm, mask);
+    if (ok) site_body<D, REAL, FMT, BND, EPI, ZS, NL>(A, par, idx, nrm, mask);
   } else {
-    if (ok) site_body<D, REAL, FMT, BND, EPI, ZS>(A, par, idx, nrm, 0u);
+    if (ok) site_body<D, REAL, FMT, BND, EPI, ZS, NL>(A, par, idx, nrm, 0u);
   }
   if constexpr (EPI != EPI_STORE) block_reduce_partial<1>(A.red, nrm);
 }
 
-template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS>
+template <int D, bool REAL, int FMT, bool BND, int EPI, bool ZS, int NL>
 __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, double (&nrm)[1], unsigned mask) {
   {
-    const int i = A.list[par] ? A.list[par][idx] : idx + A.ioff[par];
+    const int i = (NL > 0 || !A.list[par]) ? idx + A.ioff[par] : A.list[par][idx];
     int c[4], s;
     cb_coords(A.g, i, par, c, s);
+    // NL > 0: whole warps on one cb tile (host check), lane 0 stages the link tiles
+    auto ls = stage_links<D, REAL, FMT, NL>(A.gauge, A.g, par, i, s, c);
     double2 acc[4][D];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -372,8 +487,8 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
     constexpr int kPerm = LBCU_HOP_PERM >= 0 ? LBCU_HOP_PERM : (FMT == GF_SU2 || (D == 2 && !REAL)) ? 3210 : 123;
     auto dir = [&](auto Mc) {
       constexpr int MU = decltype(Mc)::value;
-      if constexpr (MU == 3 && ZS) hop_z_shared<D, REAL, FMT>(acc, A, in, par, i, s, mask);
-      else hop_mu<D, REAL, FMT, BND, MU>(acc, A, in, par, i, s, c);
+      if constexpr (MU == 3 && ZS) hop_z_shared<D, REAL, FMT>(acc, A, in, par, i, s, mask, ls);
+      else hop_mu<D, REAL, FMT, BND, MU>(acc, A, in, par, i, s, c, ls);
     };
     dir(std::integral_constant<int, kPerm / 1000>{});
     dir(std::integral_constant<int, kPerm / 100 % 10>{});
@@ -397,10 +512,6 @@ __device__ __forceinline__ void site_body(const HopArgs& A, int par, int idx, do
 // travel, each thread does its t and x hops from global memory; then the y
 // and z hops and the diagonal term read shared memory.
 constexpr int kRbRows = 8, kRbTiles = (kRbRows + 4) / 2;  // tiles per parity
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
 
 template <int D, int P0, int P1, int F0, int F1>
 __device__ __forceinline__ void project_sm(double2 (&h)[2][D], const double2* q, unsigned s5) {
@@ -467,8 +578,9 @@ __global__ void __launch_bounds__(256, MINB) hop_rowblock_kernel(const __grid_co
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) acc[k][cc] = make_double2(0.0, 0.0);
   const double2* in = A.in[par ^ 1];
-  hop_mu<D, REAL, FMT, false, 1>(acc, A, in, par, i, s, c);
-  hop_mu<D, REAL, FMT, false, 0>(acc, A, in, par, i, s, c);
+  LinkStage<D, REAL, FMT, 0> nols;
+  hop_mu<D, REAL, FMT, false, 1>(acc, A, in, par, i, s, c, nols);
+  hop_mu<D, REAL, FMT, false, 0>(acc, A, in, par, i, s, c, nols);
   // wait for the staged tiles of this stage (phase flips every second block)
   {
     unsigned done = 0;
@@ -690,10 +802,43 @@ int hop_block() {
 
 int hop_blocks(int nsites, int npar, int /*dr*/) { return (nsites + hop_block() - 1) / hop_block() * npar; }
 
+// Link tiles staged per warp (LinkStage) by the list-free, undecomposed kernels
+// of each storage format; 0 = none. Measured (profiles/r2s_sweep_ls_mix.log,
+// r2r_traffic_ls_mix.txt): the four forward tiles help the SU(3) R10/R12 hop
+// (config 3: eo hop -3 %, full Dphi -1 to -2 %; six tiles leave too little L1),
+// SU(2) links lose 2-7 % (their links shared L1 lines with the other parity)
+// and AS4R's 9 KB tiles 13 %. -DLBCU_HOP_NL=n forces one value for A/B builds
+// (tools/build_variant.sh).
+#ifndef LBCU_HOP_NL
+#define LBCU_HOP_NL -1
+#endif
+template <int D, bool REAL, int FMT, bool ZS>
+constexpr int ls_slots() {
+  if (LBCU_HOP_NL >= 0) return (LBCU_HOP_NL == 7 && !ZS) ? 6 : LBCU_HOP_NL;
+  if (FMT == GF_R10 || FMT == GF_R12) return 4;
+  return 0;
+}
+
 template <int D, bool REAL, int FMT, int MINB>
-void launch_hop_minb(const HopArgs& A, bool bnd, int epi, bool zs, int blocks, cudaStream_t s) {
+void launch_hop_minb(const HopArgs& A, bool bnd, int epi, bool zs, bool ls, int blocks, cudaStream_t s) {
 #define LBCU_HOP_CASE(B, E, Z)                                                      \
   if (bnd == B && epi == E && zs == Z) {                                            \
+    constexpr int NL = B ? 0 : ls_slots<D, REAL, FMT, Z>();                         \
+    if constexpr (NL > 0) {                                                         \
+      if (ls) {                                                                     \
+        auto* k = hop_kernel<D, REAL, FMT, B, E, MINB, Z, NL>;                      \
+        const int nw = hop_block() / 32;                                            \
+        const size_t smem = (size_t)nw * NL * LinkStage<D, REAL, FMT, NL>::TILE *   \
+                                sizeof(ElemT<D, REAL, FMT>) + nw * 8;               \
+        static bool attr = false;                                                   \
+        if (!attr) {                                                                \
+          LBCU_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+          attr = true;                                                              \
+        }                                                                           \
+        k<<<blocks, hop_block(), smem, s>>>(A);                                     \
+        return;                                                                     \
+      }                                                                             \
+    }                                                                               \
     hop_kernel<D, REAL, FMT, B, E, MINB, Z><<<blocks, hop_block(), 0, s>>>(A);      \
     return;                                                                         \
   }
@@ -714,7 +859,7 @@ void launch_hop_minb(const HopArgs& A, bool bnd, int epi, bool zs, int blocks, c
 
 template <int D, bool REAL, int FMT>
 void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaStream_t s,
-                int blocks_override = 0, bool zs = false) {
+                int blocks_override = 0, bool zs = false, bool ls = false) {
   if (nsites <= 0) return;
   // measured (profiles/r03_tune_zs_*, r03_tune_xcol_zs_*): +2.5 % for SU(2)
   // fundamental; -1.5 % (SU(3) R12), -3 % (SU(2) adjoint), -15 % (AS4R) from
@@ -724,21 +869,21 @@ void launch_hop(const HopArgs& A, bool bnd, int epi, int nsites, int npar, cudaS
   if constexpr (D <= 3) {
     const int minb = env_int("LBCU_HOP_MINB", default_minb<D, REAL, FMT>());
     if (minb == 4) {
-      launch_hop_minb<D, REAL, FMT, 4>(A, bnd, epi, zs, blocks, s);
+      launch_hop_minb<D, REAL, FMT, 4>(A, bnd, epi, zs, ls, blocks, s);
       return;
     }
     if constexpr (D == 2 && FMT == GF_SU2) {
       if (minb == 5) {
-        launch_hop_minb<D, REAL, FMT, 5>(A, bnd, epi, zs, blocks, s);
+        launch_hop_minb<D, REAL, FMT, 5>(A, bnd, epi, zs, ls, blocks, s);
         return;
       }
     }
     if (minb == 3) {
-      launch_hop_minb<D, REAL, FMT, 3>(A, bnd, epi, zs, blocks, s);
+      launch_hop_minb<D, REAL, FMT, 3>(A, bnd, epi, zs, ls, blocks, s);
       return;
     }
   }
-  launch_hop_minb<D, REAL, FMT, 1>(A, bnd, epi, zs, blocks, s);
+  launch_hop_minb<D, REAL, FMT, 1>(A, bnd, epi, zs, ls, blocks, s);
 }
 
 // Supported representation dimensions and storage formats (compile-time
@@ -847,6 +992,16 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     A.both = npar == 2;
     A.par0 = pars[0];
     int blocks = hop_blocks(A.nsites, npar, dr);
+    // full Dphi: both parities of one cb range in a block (warps 0-1 parity 0,
+    // warps 2-3 parity 1), so a block's diagonal, z and y operands and its y and
+    // z links are the other half's neighbour operands and meet in L1: L2 -> SM
+    // bytes -9 %, time -1.4 to -3 % on configs 2-5 (profiles/r2r_traffic_ls_mix.txt)
+    const bool mix = npar == 2 && env_int("LBCU_HOP_MIX", 1) && hop_block() % 64 == 0;
+    const int bsz = mix ? hop_block() / 2 : hop_block();
+    if (mix) {
+      A.both = 2;
+      blocks = (A.nsites + bsz - 1) / bsz;
+    }
     // L2-blocked schedule: spatial blocks of bx x-planes whose two-slice
     // working set (spinor in/out + links as stored) fits the L2 budget
     if (env_int("LBCU_HOP_SCHED", 1)) {
@@ -861,8 +1016,8 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
       if (bx < geo.local[1]) {  // a whole slice fits: the linear order is the same sweep
         A.sched_bx = bx;
         A.sched_len = bx * geo.local[2] * geo.local[3] / 2;
-        A.sched_cpb = (A.sched_len + hop_block() - 1) / hop_block();
-        blocks = (geo.local[1] / bx) * geo.local[0] * A.sched_cpb * npar;
+        A.sched_cpb = (A.sched_len + bsz - 1) / bsz;
+        blocks = (geo.local[1] / bx) * geo.local[0] * A.sched_cpb * (mix ? 1 : npar);
       }
     }
     if (reduce) {
@@ -890,8 +1045,11 @@ void hop_apply(lbcu_ctx_s* ctx, const HopCall& c) {
     // warp-shared z hops when every warp covers whole z-rows (hop_z_shared)
     const int hz = geo.local[3] / 2;
     const bool zs = env_int("LBCU_HOP_ZS", 1) && hz > 0 && 32 % hz == 0;
+    // link staging (LinkStage): every warp must sit on one cb tile of one x-plane
+    const bool ls = env_int("LBCU_HOP_LS", 1) && (geo.local[2] * geo.local[3] / 2) % kTile == 0 &&
+                    hop_block() % kTile == 0;
     dispatch(dr, real, fmt, [&](auto Dc, auto Rc, auto Fc) {
-      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s, blocks, zs);
+      launch_hop<LBCU_TPARAMS(Dc, Rc, Fc)>(A, false, c.epi, A.nsites, npar, s, blocks, zs, ls);
     });
     ctx->launches += 1;
     if (reduce) {

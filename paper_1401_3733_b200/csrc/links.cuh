@@ -52,9 +52,12 @@ namespace lbcu {
 // Link loads: the read-only path. (L1::no_allocate hints, to leave L1 to the
 // neighbour spinors, measured 0-8 % slower: the full Dphi's two parities
 // share links through L1.)
-template <class T>
+// SM = true: the entry sits in a shared-memory tile staged by a bulk async
+// copy (dslash.cu, link staging), read with a plain load.
+template <bool SM = false, class T>
 __device__ __forceinline__ T ldlink(const T* p) {
-  return __ldg(p);
+  if constexpr (SM) return *p;
+  else return __ldg(p);
 }
 
 enum GaugeFmt { GF_FULL = 0, GF_SU2 = 1, GF_R12 = 2, GF_AS4 = 3, GF_AS4R = 4, GF_R10 = 5 };
@@ -233,24 +236,24 @@ __device__ __forceinline__ void build_link(LinkT<REAL> (&u)[D * D],
 }
 
 // Load a link from its storage (read-only path) and rebuild it.
-template <int D, bool REAL, int FMT>
+template <int D, bool REAL, int FMT, bool SM = false>
 __device__ __forceinline__ void load_link(LinkT<REAL> (&u)[D * D],
                                           const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
                                           long long st) {
   if constexpr (FMT == GF_FULL) {
 #pragma unroll
-    for (int e = 0; e < D * D; ++e) u[e] = ldlink(p + (long long)e * st);
+    for (int e = 0; e < D * D; ++e) u[e] = ldlink<SM>(p + (long long)e * st);
   } else {
     double2 s[LinkFmt<D, REAL, FMT>::entries];
 #pragma unroll
-    for (int e = 0; e < LinkFmt<D, REAL, FMT>::entries; ++e) s[e] = ldlink(p + (long long)e * st);
+    for (int e = 0; e < LinkFmt<D, REAL, FMT>::entries; ++e) s[e] = ldlink<SM>(p + (long long)e * st);
     build_link<D, REAL, FMT>(u, s);
   }
 }
 
 // GF_AS4R: g' = M hp with M = R' (or R'^T for the dagger), all in the Wt
 // basis; the link is streamed one stored row (3 double2) at a time.
-template <bool DAG>
+template <bool DAG, bool SM = false>
 __device__ __forceinline__ void as4r_mul(double2 (&g)[2][6], const double2* __restrict__ p, long long st,
                                          const double2 (&hp)[2][6]) {
 #pragma unroll
@@ -260,7 +263,7 @@ __device__ __forceinline__ void as4r_mul(double2 (&g)[2][6], const double2* __re
     double m[6];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const double2 v = ldlink(p + (long long)(3 * r + q) * st);
+      const double2 v = ldlink<SM>(p + (long long)(3 * r + q) * st);
       m[2 * q] = v.x;
       m[2 * q + 1] = v.y;
     }
@@ -278,7 +281,7 @@ __device__ __forceinline__ void as4r_mul(double2 (&g)[2][6], const double2* __re
 }
 
 // g[a][r] = sum_c M_rc h[a][c] with M = U (DAG = false) or U^dag (DAG = true)
-template <int D, bool REAL, int FMT, bool DAG>
+template <int D, bool REAL, int FMT, bool DAG, bool SM = false>
 __device__ __forceinline__ void link_mul(double2 (&g)[2][D],
                                          const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
                                          long long st, const double2 (&h)[2][D]) {
@@ -286,7 +289,7 @@ __device__ __forceinline__ void link_mul(double2 (&g)[2][D],
     double2 hp[2][6];
     as4r_in(hp[0], h[0]);
     as4r_in(hp[1], h[1]);
-    as4r_mul<DAG>(g, p, st, hp);
+    as4r_mul<DAG, SM>(g, p, st, hp);
     as4r_out(g[0], 0.5);
     as4r_out(g[1], 0.5);
     return;
@@ -299,7 +302,7 @@ __device__ __forceinline__ void link_mul(double2 (&g)[2][D],
     for (int r = 0; r < D; ++r)
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const auto u = ldlink(p + (long long)(DAG ? c * D + r : r * D + c) * st);
+        const auto u = ldlink<SM>(p + (long long)(DAG ? c * D + r : r * D + c) * st);
         if constexpr (REAL) {
           rmac(g[0][r], u, h[0][c]);
           rmac(g[1][r], u, h[1][c]);
@@ -313,7 +316,7 @@ __device__ __forceinline__ void link_mul(double2 (&g)[2][D],
       }
   } else {
     LinkT<REAL> u[D * D];
-    load_link<D, REAL, FMT>(u, p, st);
+    load_link<D, REAL, FMT, SM>(u, p, st);
 #pragma unroll
     for (int r = 0; r < D; ++r)
 #pragma unroll
@@ -337,7 +340,7 @@ __device__ __forceinline__ void link_mul(double2 (&g)[2][D],
 //   g_a = sum_c M_rc h[a][c]  (a = 0, 1), then
 //   acc[0][r] += g_0; acc[1][r] += g_1; acc[2][r] += Q0 g_R0; acc[3][r] += Q1 g_R1
 // so the 2 x D intermediate g never has to be held in registers.
-template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1>
+template <int D, bool REAL, int FMT, bool DAG, int R0, int R1, int Q0, int Q1, bool SM = false>
 __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
                                              const typename LinkFmt<D, REAL, FMT>::Elem* __restrict__ p,
                                              long long st, const double2 (&h)[2][D]) {
@@ -345,7 +348,7 @@ __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
     double2 hp[2][6], g[2][6];
     as4r_in(hp[0], h[0]);
     as4r_in(hp[1], h[1]);
-    as4r_mul<DAG>(g, p, st, hp);
+    as4r_mul<DAG, SM>(g, p, st, hp);
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
       acc[0][r] = cadd(acc[0][r], g[0][r]);
@@ -359,7 +362,7 @@ __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
     // keep only the fundamental element in registers; form each minor when used
     double2 s[16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) s[e] = ldlink(p + (long long)e * st);
+    for (int e = 0; e < 16; ++e) s[e] = ldlink<SM>(p + (long long)e * st);
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
       double2 g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
@@ -385,7 +388,7 @@ __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
     return;
   }
   [[maybe_unused]] LinkT<REAL> u[FMT == GF_FULL ? 1 : D * D];
-  if constexpr (FMT != GF_FULL) load_link<D, REAL, FMT>(u, p, st);
+  if constexpr (FMT != GF_FULL) load_link<D, REAL, FMT, SM>(u, p, st);
 #pragma unroll
   for (int r = 0; r < D; ++r) {
     double2 g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
@@ -393,7 +396,7 @@ __device__ __forceinline__ void link_mul_acc(double2 (&acc)[4][D],
     for (int c = 0; c < D; ++c) {
       const int idx = DAG ? c * D + r : r * D + c;
       LinkT<REAL> e;
-      if constexpr (FMT == GF_FULL) e = ldlink(p + (long long)idx * st);
+      if constexpr (FMT == GF_FULL) e = ldlink<SM>(p + (long long)idx * st);
       else e = u[idx];
       if constexpr (REAL) {
         rmac(g0, e, h[0][c]);
