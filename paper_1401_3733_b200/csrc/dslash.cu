@@ -804,18 +804,19 @@ int hop_blocks(int nsites, int npar, int /*dr*/) { return (nsites + hop_block() 
 
 // Link tiles staged per warp (LinkStage) by the list-free, undecomposed kernels
 // of each storage format; 0 = none. Measured (profiles/r2s_sweep_ls_mix.log,
-// r2r_traffic_ls_mix.txt): the four forward tiles help the SU(3) R10/R12 hop
-// (config 3: eo hop -3 %, full Dphi -1 to -2 %; six tiles leave too little L1),
-// SU(2) links lose 2-7 % (their links shared L1 lines with the other parity)
-// and AS4R's 9 KB tiles 13 %. -DLBCU_HOP_NL=n forces one value for A/B builds
-// (tools/build_variant.sh).
+// r2r_traffic_ls_mix.txt, r2x_ls_r12_balance.log): the four forward tiles help
+// the SU(3) R10 hop (config 3: eo hop -3 to -4 %, eo CG -2 %, full Dphi -0.5 %;
+// six tiles leave too little L1); R12's 3 KB tiles cost the full Dphi 8-11 %
+// for 1-2 % on the eo hop, SU(2) links lose 2-7 % (their links shared L1 lines
+// with the other parity) and AS4R's 9 KB tiles 13 %. -DLBCU_HOP_NL=n forces one
+// value for A/B builds (tools/build_variant.sh).
 #ifndef LBCU_HOP_NL
 #define LBCU_HOP_NL -1
 #endif
 template <int D, bool REAL, int FMT, bool ZS>
 constexpr int ls_slots() {
   if (LBCU_HOP_NL >= 0) return (LBCU_HOP_NL == 7 && !ZS) ? 6 : LBCU_HOP_NL;
-  if (FMT == GF_R10 || FMT == GF_R12) return 4;
+  if (FMT == GF_R10) return 4;
   return 0;
 }
 
